@@ -1,0 +1,164 @@
+/*
+ * bsparse.h -- C ABI of libbsparse.so, the B200 (sm_100a) back end for the
+ * hot path of the hybrid sparse matrix of arXiv 1805.03380 (reference:
+ * autosparse, /root/reference/pkg/src/autosparse).
+ *
+ * Conventions:
+ *  - every pointer argument is a DEVICE pointer unless marked (host);
+ *  - indices on device are int32, col_ptr int32[n_cols+1]; values float64 (_f64)
+ *    or float32 (_f32);
+ *  - outputs are caller-allocated; outputs whose size is data dependent take
+ *    a capacity upper bound and report the realised size in info[0] (device);
+ *  - scratch comes from the caller (`ws`, `ws_bytes`, sized by the matching
+ *    *_workspace_bytes function); the library never allocates or frees;
+ *  - all work is enqueued on `stream` (a cudaStream_t); no call synchronises
+ *    except where stated;
+ *  - every function returns an as_status code; as_last_error() describes the
+ *    last failure of the calling thread.
+ *
+ * Each entry point names the reference interface it replaces.
+ */
+#ifndef BSPARSE_H_
+#define BSPARSE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum as_status {
+  AS_OK = 0,
+  AS_ERR_SHAPE = 1,   /* errors.ShapeError            (errors.py:14-21) */
+  AS_ERR_COORD = 2,   /* errors.CoordinateError       (errors.py:7-8)   */
+  AS_ERR_CORRUPT = 3, /* errors.CorruptionError       (errors.py:10-11) */
+  AS_ERR_CUDA = 4,    /* CUDA runtime failure; see as_last_error()       */
+  AS_ERR_ARG = 5      /* bad argument (null pointer, workspace too small, size limits) */
+};
+
+enum as_dup { AS_DUP_SUM = 0, AS_DUP_LAST = 1 }; /* csc.DUP_SUM / DUP_LAST (csc.py:20-21) */
+
+const char *as_last_error(void);
+int as_abi_version(void);
+
+/* ---------------------------------------------------------------------------
+ * COO triplets -> canonical CSC.
+ * Replaces csc.canonicalize (csc.py:148-193) and, with the range check,
+ * csc.from_triplets (csc.py:208-222) / coo.to_csc (coo.py:51-62).
+ * rows/cols are int32 (idx_bytes == 4) or int64 (idx_bytes == 8).  Outputs
+ * are sized for n (nnz <= n).  info[0] = nnz, info[1] = index of the first
+ * out-of-range triplet or a value >= n when all are in range (the kernels
+ * skip bad triplets; the caller raises CoordinateError naming info[1]).
+ */
+size_t as_build_workspace_bytes(int64_t n, int64_t n_cols);
+int as_coo_to_csc_f64(int64_t n_rows, int64_t n_cols, int64_t n, const void *rows, const void *cols,
+                      int idx_bytes, const double *vals, int dup, int32_t *col_ptr, int32_t *row_idx,
+                      double *out_vals, int64_t *info, void *ws, size_t ws_bytes, void *stream);
+int as_coo_to_csc_f32(int64_t n_rows, int64_t n_cols, int64_t n, const void *rows, const void *cols,
+                      int idx_bytes, const float *vals, int dup, int32_t *col_ptr, int32_t *row_idx,
+                      float *out_vals, int64_t *info, void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Insertion-cache flush: base CSC + element-write log -> canonical CSC.
+ * Replaces rbt.to_csc (rbt.py:444-458) of the tree that RbtStore.insert
+ * (rbt.py:371-387: overwrite; 0.0 erases, :374-376) built on top of
+ * rbt.from_csc(base) (rbt.py:461-476).  Last write wins, exact zeros erase.
+ * Outputs sized for nnz_base + n_log.  info[0] = nnz, info[1] as above.
+ */
+size_t as_flush_workspace_bytes(int64_t nnz_base, int64_t n_log, int64_t n_cols);
+int as_flush_log_f64(int64_t n_rows, int64_t n_cols, int64_t nnz_base, const int32_t *base_col_ptr,
+                     const int32_t *base_row_idx, const double *base_vals, int64_t n_log,
+                     const int32_t *log_rows, const int32_t *log_cols, const double *log_vals,
+                     int32_t *col_ptr, int32_t *row_idx, double *out_vals, int64_t *info, void *ws,
+                     size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * CSC transpose.  Replaces _kernels.transpose (_kernels.py:130-150) via
+ * ops.transpose (ops.py:123-128).  Output: CSC of A^T, n_rows+1 offsets,
+ * nnz entries, rows sorted within each column (stable order of the reference).
+ */
+size_t as_transpose_workspace_bytes(int64_t nnz, int64_t n_rows);
+int as_csc_transpose_f64(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t *col_ptr,
+                         const int32_t *row_idx, const double *vals, int32_t *t_col_ptr,
+                         int32_t *t_row_idx, double *t_vals, void *ws, size_t ws_bytes, void *stream);
+int as_csc_transpose_f32(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t *col_ptr,
+                         const int32_t *row_idx, const float *vals, int32_t *t_col_ptr,
+                         int32_t *t_row_idx, float *t_vals, void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * alpha*A + beta*B.  Replaces _kernels.linear_combine (_kernels.py:12-48) via
+ * ops._combine/add/subtract/scaled_sum (ops.py:50-73).  Products and the sum
+ * are separately rounded (no FMA), exact zeros pruned.  nnz_a/nnz_b (host)
+ * size the launch.  Outputs sized for nnz_a + nnz_b; info[0] = nnz.
+ */
+size_t as_add_workspace_bytes(int64_t n_cols, int64_t nnz_a, int64_t nnz_b);
+int as_csc_add_f64(int64_t n_rows, int64_t n_cols, double alpha, double beta, const int32_t *a_col_ptr,
+                   const int32_t *a_row_idx, const double *a_vals, const int32_t *b_col_ptr,
+                   const int32_t *b_row_idx, const double *b_vals, int64_t nnz_a, int64_t nnz_b,
+                   int32_t *col_ptr, int32_t *row_idx, double *out_vals, int64_t *info, void *ws,
+                   size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * SpGEMM C = A @ B (Gustavson, bit-exact accumulation order).  Replaces
+ * _kernels.spgemm (_kernels.py:51-103) via ops.matmul (ops.py:110-120).
+ * Two phases: as_spgemm_products writes prod_ptr (int64[n_cols_b+1], the
+ * per-column product counts' prefix sum) and info[0] = total products, an
+ * upper bound of nnz(C); as_spgemm_f64 then fills outputs sized for that
+ * bound, info[0] = nnz.  prod_ptr must be kept between the calls.
+ */
+size_t as_spgemm_products_workspace_bytes(int64_t n_cols_b);
+int as_spgemm_products(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int32_t *a_col_ptr,
+                       const int32_t *b_col_ptr, const int32_t *b_row_idx, int64_t *prod_ptr, int64_t *info,
+                       void *ws, size_t ws_bytes, void *stream);
+size_t as_spgemm_workspace_bytes(int64_t n_cols_b, int64_t total_products);
+int as_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int32_t *a_col_ptr,
+                  const int32_t *a_row_idx, const double *a_vals, const int32_t *b_col_ptr,
+                  const int32_t *b_row_idx, const double *b_vals, const int64_t *prod_ptr,
+                  int64_t total_products, int32_t *col_ptr, int32_t *row_idx, double *out_vals,
+                  int64_t *info, void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * SpMM C = A @ B with dense column-major B (n_cols x k, ldb) and C
+ * (n_rows x k, ldc).  A is given in CSR form, i.e. the CSC arrays of A^T
+ * (row_ptr[n_rows+1], col_idx, vals), which the hybrid handle caches.  The
+ * reference API has only the k = 1 case, _kernels.mat_times_vec
+ * (_kernels.py:118-127) via ops.mat_times_vec (ops.py:97-107); its oracle
+ * for k > 1 is k such calls.
+ *  exact != 0: per output entry a float64 left fold in column order with
+ *              separately rounded products, columns with B[j,c] == 0 skipped
+ *              -- bit-identical to the reference for float64 data;
+ *  exact == 0: float32 FMA accumulation (tolerance 1e-5, float32 only).
+ * ws: as_spmm_workspace_bytes (one row-major chunk of B).
+ */
+size_t as_spmm_workspace_bytes(int64_t n_cols, int64_t k, int dtype_bytes);
+int as_spmm_csr_f32(int64_t n_rows, int64_t n_cols, int64_t k, const int32_t *row_ptr,
+                    const int32_t *col_idx, const float *vals, const float *B, int64_t ldb, float *C,
+                    int64_t ldc, int exact, void *ws, size_t ws_bytes, void *stream);
+int as_spmm_csr_f64(int64_t n_rows, int64_t n_cols, int64_t k, const int32_t *row_ptr,
+                    const int32_t *col_idx, const double *vals, const double *B, int64_t ldb, double *C,
+                    int64_t ldc, void *ws, size_t ws_bytes, void *stream);
+
+/* w = v^T A.  Replaces _kernels.vec_times_mat (_kernels.py:106-115). */
+int as_vecmat_csc_f64(int64_t n_rows, int64_t n_cols, const int32_t *col_ptr, const int32_t *row_idx,
+                      const double *vals, const double *v, double *w, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * trace(A^T B) without forming the product: sum over coincident nonzeros.
+ * Replaces _kernels.fused_trace (_kernels.py:153-175) via
+ * expr.fused_trace_at_b (expr.py:197-209).
+ * nnz_a/nnz_b (host) size the launch.  out[0] = the sum, out[1] = its
+ * double-double residual (partials of column slices combine exactly, used by
+ * the multi-GPU path).  Deterministic.  ws: as_trace_workspace_bytes.
+ */
+size_t as_trace_workspace_bytes(int64_t n_cols, int64_t nnz_a, int64_t nnz_b);
+int as_trace_atb_f64(int64_t n_rows, int64_t n_cols, const int32_t *a_col_ptr, const int32_t *a_row_idx,
+                     const double *a_vals, const int32_t *b_col_ptr, const int32_t *b_row_idx,
+                     const double *b_vals, int64_t nnz_a, int64_t nnz_b, double *out, void *ws,
+                     size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BSPARSE_H_ */

@@ -1,0 +1,217 @@
+"""Device kernels over flat CSC arrays -- the B200 replacement of the
+reference's flat-array kernel module (autosparse/_kernels.py:1-175,
+csc.canonicalize csc.py:148-193, rbt.to_csc rbt.py:444-458).
+
+Arrays are torch CUDA tensors: indices int32, values float64 (or float32
+where noted), col_ptr int32[n_cols+1].  Every function launches the
+sm_100a kernels of libbsparse.so on the current stream; outputs whose size
+is data dependent are sized on the device and read back with one 16-byte
+device->host copy (the only synchronisation).  There is no CPU path.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._lib import check, ptr, stream, workspace
+
+DUP_SUM = "sum"
+DUP_LAST = "last"
+_DUP = {DUP_SUM: _lib.AS_DUP_SUM, DUP_LAST: _lib.AS_DUP_LAST}
+
+
+def _dev(device=None):
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def _read_info(info):
+    nnz, bad = (int(x) for x in info.cpu().tolist())
+    return nnz, bad
+
+
+def coo_to_csc(n_rows, n_cols, rows, cols, vals, dup=DUP_SUM):
+    """Canonical CSC from COO triplets (csc.canonicalize, csc.py:148-193):
+    stable column-major order, duplicates summed in np.add.reduceat order or
+    last-wins, exact zeros pruned.  rows/cols int32 or int64 on the device.
+    Returns (col_ptr, row_idx, vals, first_bad) where first_bad is the index
+    of the first out-of-range triplet or None (those are skipped)."""
+    L = _lib.lib()
+    dev = vals.device
+    n = int(vals.shape[0])
+    assert rows.dtype == cols.dtype and rows.dtype in (torch.int32, torch.int64)
+    idx_bytes = 4 if rows.dtype == torch.int32 else 8
+    f = L.as_coo_to_csc_f64 if vals.dtype == torch.float64 else L.as_coo_to_csc_f32
+    col_ptr = torch.empty(n_cols + 1, dtype=torch.int32, device=dev)
+    row_idx = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    out_vals = torch.empty(max(n, 1), dtype=vals.dtype, device=dev)
+    info = torch.empty(2, dtype=torch.int64, device=dev)
+    ws_bytes = L.as_build_workspace_bytes(n, n_cols)
+    ws = workspace(ws_bytes, dev)
+    check(f(n_rows, n_cols, n, ptr(rows), ptr(cols), idx_bytes, ptr(vals), _DUP[dup], ptr(col_ptr), ptr(row_idx),
+            ptr(out_vals), ptr(info), ptr(ws), ws_bytes, stream()))
+    nnz, bad = _read_info(info)
+    return col_ptr, row_idx[:nnz], out_vals[:nnz], (bad if bad < n else None)
+
+
+def flush_log(n_rows, n_cols, base, log_rows, log_cols, log_vals):
+    """Insertion-cache flush (rbt.to_csc over RbtStore semantics,
+    rbt.py:371-458): base CSC (col_ptr, row_idx, vals) overwritten by the write
+    log in order; last write wins, a 0.0 write erases.  log_* int32 / float64.
+    Returns (col_ptr, row_idx, vals, first_bad_log_index_or_None)."""
+    L = _lib.lib()
+    b_ptr, b_rows, b_vals = base
+    dev = b_ptr.device
+    nb = int(b_rows.shape[0])
+    nl = int(log_vals.shape[0])
+    cap = max(nb + nl, 1)
+    col_ptr = torch.empty(n_cols + 1, dtype=torch.int32, device=dev)
+    row_idx = torch.empty(cap, dtype=torch.int32, device=dev)
+    out_vals = torch.empty(cap, dtype=torch.float64, device=dev)
+    info = torch.empty(2, dtype=torch.int64, device=dev)
+    ws_bytes = L.as_flush_workspace_bytes(nb, nl, n_cols)
+    ws = workspace(ws_bytes, dev)
+    check(L.as_flush_log_f64(n_rows, n_cols, nb, ptr(b_ptr), ptr(b_rows), ptr(b_vals), nl, ptr(log_rows),
+                             ptr(log_cols), ptr(log_vals), ptr(col_ptr), ptr(row_idx), ptr(out_vals), ptr(info),
+                             ptr(ws), ws_bytes, stream()))
+    nnz, bad = _read_info(info)
+    return col_ptr, row_idx[:nnz], out_vals[:nnz], (bad if bad < nl else None)
+
+
+def transpose(n_rows, n_cols, col_ptr, row_idx, vals):
+    """CSC of A^T (_kernels.transpose, _kernels.py:130-150).  No sync."""
+    L = _lib.lib()
+    dev = col_ptr.device
+    nnz = int(row_idx.shape[0])
+    t_ptr = torch.empty(n_rows + 1, dtype=torch.int32, device=dev)
+    t_rows = torch.empty(nnz, dtype=torch.int32, device=dev)
+    t_vals = torch.empty(nnz, dtype=vals.dtype, device=dev)
+    ws_bytes = L.as_transpose_workspace_bytes(nnz, n_rows)
+    ws = workspace(ws_bytes, dev)
+    f = L.as_csc_transpose_f64 if vals.dtype == torch.float64 else L.as_csc_transpose_f32
+    check(f(n_rows, n_cols, nnz, ptr(col_ptr), ptr(row_idx), ptr(vals), ptr(t_ptr), ptr(t_rows), ptr(t_vals),
+            ptr(ws), ws_bytes, stream()))
+    return t_ptr, t_rows, t_vals
+
+
+def linear_combine(n_rows, n_cols, a, b, alpha, beta):
+    """alpha*A + beta*B (_kernels.linear_combine, _kernels.py:12-48)."""
+    L = _lib.lib()
+    a_ptr, a_rows, a_vals = a
+    b_ptr, b_rows, b_vals = b
+    dev = a_ptr.device
+    na, nb = int(a_rows.shape[0]), int(b_rows.shape[0])
+    cap = max(na + nb, 1)
+    col_ptr = torch.empty(n_cols + 1, dtype=torch.int32, device=dev)
+    row_idx = torch.empty(cap, dtype=torch.int32, device=dev)
+    out_vals = torch.empty(cap, dtype=torch.float64, device=dev)
+    info = torch.zeros(2, dtype=torch.int64, device=dev)
+    ws_bytes = L.as_add_workspace_bytes(n_cols, na, nb)
+    ws = workspace(ws_bytes, dev)
+    check(L.as_csc_add_f64(n_rows, n_cols, float(alpha), float(beta), ptr(a_ptr), ptr(a_rows), ptr(a_vals),
+                           ptr(b_ptr), ptr(b_rows), ptr(b_vals), na, nb, ptr(col_ptr), ptr(row_idx), ptr(out_vals),
+                           ptr(info), ptr(ws), ws_bytes, stream()))
+    nnz = int(info[0].item())
+    return col_ptr, row_idx[:nnz], out_vals[:nnz]
+
+
+def spgemm_products(n_rows_a, n_inner, n_cols_b, a_ptr, b_ptr, b_rows):
+    """Per-column product counts' prefix sum (int64[n_cols_b+1]) and total."""
+    L = _lib.lib()
+    dev = a_ptr.device
+    prod_ptr = torch.empty(n_cols_b + 1, dtype=torch.int64, device=dev)
+    info = torch.zeros(2, dtype=torch.int64, device=dev)
+    ws_bytes = L.as_spgemm_products_workspace_bytes(n_cols_b)
+    ws = workspace(ws_bytes, dev)
+    check(L.as_spgemm_products(n_rows_a, n_inner, n_cols_b, ptr(a_ptr), ptr(b_ptr), ptr(b_rows), ptr(prod_ptr),
+                               ptr(info), ptr(ws), ws_bytes, stream()))
+    return prod_ptr, int(info[0].item())
+
+
+def spgemm(n_rows_a, n_inner, n_cols_b, a, b):
+    """C = A @ B (_kernels.spgemm, _kernels.py:51-103), bit-exact order."""
+    L = _lib.lib()
+    a_ptr, a_rows, a_vals = a
+    b_ptr, b_rows, b_vals = b
+    dev = a_ptr.device
+    prod_ptr, total = spgemm_products(n_rows_a, n_inner, n_cols_b, a_ptr, b_ptr, b_rows)
+    cap = max(total, 1)
+    col_ptr = torch.empty(n_cols_b + 1, dtype=torch.int32, device=dev)
+    row_idx = torch.empty(cap, dtype=torch.int32, device=dev)
+    out_vals = torch.empty(cap, dtype=torch.float64, device=dev)
+    info = torch.zeros(2, dtype=torch.int64, device=dev)
+    ws_bytes = L.as_spgemm_workspace_bytes(n_cols_b, total)
+    ws = workspace(ws_bytes, dev)
+    check(L.as_spgemm_f64(n_rows_a, n_inner, n_cols_b, ptr(a_ptr), ptr(a_rows), ptr(a_vals), ptr(b_ptr), ptr(b_rows),
+                          ptr(b_vals), ptr(prod_ptr), total, ptr(col_ptr), ptr(row_idx), ptr(out_vals), ptr(info),
+                          ptr(ws), ws_bytes, stream()))
+    nnz = int(info[0].item())
+    return col_ptr, row_idx[:nnz], out_vals[:nnz]
+
+
+def as_col_major(B):
+    """(rows, k) tensor with unit row stride (Fortran order), and its ld."""
+    if B.dim() == 1:
+        return B.contiguous().view(-1, 1), max(int(B.shape[0]), 1)
+    if B.stride(0) != 1 or B.stride(1) < max(B.shape[0], 1):
+        B = B.t().contiguous().t()
+    return B, int(B.stride(1)) if B.shape[1] > 1 else max(int(B.shape[0]), 1)
+
+
+def spmm(n_rows, n_cols, csr, B, exact=None, out=None):
+    """C = A @ B for dense column-major B (n_cols x k) using the CSR of A
+    (= CSC arrays of A^T).  float64: exact (bit-identical to k calls of
+    mat_times_vec, _kernels.py:118-127).  float32: FMA accumulation unless
+    exact=True (float64 accumulation, one rounding at the end)."""
+    L = _lib.lib()
+    r_ptr, c_idx, vals = csr
+    dev = r_ptr.device
+    B, ldb = as_col_major(B)
+    k = int(B.shape[1])
+    if out is None:
+        C = torch.empty((k, n_rows), dtype=vals.dtype, device=dev).t()
+    else:
+        C = out
+    ldc = int(C.stride(1)) if k > 1 else max(n_rows, 1)
+    ws_bytes = L.as_spmm_workspace_bytes(n_cols, k, vals.element_size())
+    ws = workspace(ws_bytes, dev)
+    if vals.dtype == torch.float64:
+        check(L.as_spmm_csr_f64(n_rows, n_cols, k, ptr(r_ptr), ptr(c_idx), ptr(vals), ptr(B), ldb, ptr(C), ldc,
+                                ptr(ws), ws_bytes, stream()))
+    else:
+        check(L.as_spmm_csr_f32(n_rows, n_cols, k, ptr(r_ptr), ptr(c_idx), ptr(vals), ptr(B), ldb, ptr(C), ldc,
+                                1 if exact else 0, ptr(ws), ws_bytes, stream()))
+    return C
+
+
+def mat_times_vec(n_rows, n_cols, csr, x):
+    """y = A x (_kernels.mat_times_vec, _kernels.py:118-127), bit-exact."""
+    return spmm(n_rows, n_cols, csr, x.view(-1, 1), exact=True).reshape(-1)
+
+
+def vec_times_mat(n_rows, n_cols, csc, v):
+    """w = v^T A (_kernels.vec_times_mat, _kernels.py:106-115), bit-exact."""
+    L = _lib.lib()
+    c_ptr, r_idx, vals = csc
+    w = torch.empty(n_cols, dtype=torch.float64, device=c_ptr.device)
+    check(L.as_vecmat_csc_f64(n_rows, n_cols, ptr(c_ptr), ptr(r_idx), ptr(vals), ptr(v), ptr(w), stream()))
+    return w
+
+
+def fused_trace(n_rows, n_cols, a, b, out=None):
+    """trace(A^T B) (_kernels.fused_trace, _kernels.py:153-175) as a device
+    tensor [sum, residual] (double-double); no sync."""
+    L = _lib.lib()
+    a_ptr, a_rows, a_vals = a
+    b_ptr, b_rows, b_vals = b
+    dev = a_ptr.device
+    na, nb = int(a_rows.shape[0]), int(b_rows.shape[0])
+    if out is None:
+        out = torch.empty(2, dtype=torch.float64, device=dev)
+    ws_bytes = L.as_trace_workspace_bytes(n_cols, na, nb)
+    ws = workspace(ws_bytes, dev)
+    check(L.as_trace_atb_f64(n_rows, n_cols, ptr(a_ptr), ptr(a_rows), ptr(a_vals), ptr(b_ptr), ptr(b_rows),
+                             ptr(b_vals), na, nb, ptr(out), ptr(ws), ws_bytes, stream()))
+    return out

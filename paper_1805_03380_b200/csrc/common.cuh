@@ -1,0 +1,249 @@
+// common.cuh -- shared device utilities for the sm_100a sparse hot path.
+//
+// Block/warp scans, the single-pass chained-scan (decoupled look-back) tile
+// state used by every kernel whose output size is only known after it runs,
+// the numpy pairwise-sum emulation that makes duplicate sums bit-exact with
+// the reference's np.add.reduceat (csc.py:179), and small index helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifndef AS_DEVICE_INLINE
+#define AS_DEVICE_INLINE __device__ __forceinline__
+#endif
+
+namespace as {
+
+constexpr int kWarp = 32;
+
+// ------------------------------------------------------------------------
+// reduce modes for runs of equal (segment, row) keys
+enum ReduceMode : int {
+  kSumPairwise = 0,  // np.add.reduceat order: v0 + pairwise(v1..)  (csc.py:179)
+  kLast = 1,         // LastWins: last in input order (csc.py:181-182, rbt.py:115-117)
+  kSumSeq = 2,       // sequential left fold (Gustavson accumulator, _kernels.py:83-93)
+};
+
+// ------------------------------------------------------------------------
+// warp / block scans (inclusive and exclusive) over 32- or 64-bit values
+template <class T>
+AS_DEVICE_INLINE T warp_inclusive_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+template <class T>
+AS_DEVICE_INLINE T warp_reduce_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide exclusive scan; every thread must call.  `smem` needs
+// (blockDim.x/32 + 1) elements.  Returns the exclusive prefix of `v`, and the
+// block total in *total.
+template <class T>
+__device__ T block_exclusive_scan(T v, T* smem, T* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+  T inc = warp_inclusive_scan(v);
+  if (lane == 31) smem[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T w = lane < nwarps ? smem[lane] : T(0);
+    T wi = warp_inclusive_scan(w);
+    if (lane < nwarps) smem[lane] = wi - w;
+    if (lane == nwarps - 1) smem[nwarps] = wi;
+  }
+  __syncthreads();
+  T res = smem[warp] + inc - v;
+  *total = smem[nwarps];
+  __syncthreads();
+  return res;
+}
+
+template <class T>
+__device__ T block_reduce_sum(T v, T* smem) {
+  T total;
+  (void)block_exclusive_scan(v, smem, &total);
+  return total;
+}
+
+// ------------------------------------------------------------------------
+// Chained scan (single-pass decoupled look-back).  One 64-bit word per tile:
+// (value << 2) | flag, flag 1 = tile aggregate, 2 = inclusive prefix.
+// The tile state array and the ticket counter must be zeroed before launch.
+constexpr unsigned long long kFlagAgg = 1ull, kFlagInc = 2ull;
+
+AS_DEVICE_INLINE void tile_publish(unsigned long long* st, unsigned long long value,
+                                   unsigned long long flag) {
+  __threadfence();
+  atomicExch(st, (value << 2) | flag);
+}
+
+AS_DEVICE_INLINE unsigned long long tile_peek(const unsigned long long* st) {
+  return *((volatile const unsigned long long*)st);
+}
+
+// Executed by one full warp of the tile.  Returns the exclusive prefix of
+// tile `t` after publishing its aggregate and, then, its inclusive prefix.
+__device__ inline unsigned long long tile_lookback_warp(unsigned long long* states, long long t,
+                                                        unsigned long long aggregate) {
+  const int lane = threadIdx.x & 31;
+  if (t == 0) {
+    if (lane == 0) tile_publish(&states[0], aggregate, kFlagInc);
+    return 0;
+  }
+  if (lane == 0) tile_publish(&states[t], aggregate, kFlagAgg);
+  unsigned long long prefix = 0;
+  long long base = t - 1;
+  while (true) {
+    long long i = base - lane;
+    unsigned long long s = 0;
+    if (i >= 0) {
+      do {
+        s = tile_peek(&states[i]);
+      } while ((s & 3ull) == 0ull);
+    } else {
+      s = kFlagInc;  // virtual inclusive 0 before tile 0
+    }
+    unsigned inc_mask = __ballot_sync(0xffffffffu, (s & 3ull) == kFlagInc);
+    // lanes up to and including the first inclusive one contribute
+    int first = inc_mask ? (__ffs(inc_mask) - 1) : 32;
+    unsigned long long v = (lane <= first) ? (s >> 2) : 0ull;
+    prefix += warp_reduce_sum(v);
+    if (inc_mask) break;
+    base -= 32;
+  }
+  __threadfence();
+  if (lane == 0) tile_publish(&states[t], prefix + aggregate, kFlagInc);
+  return prefix;
+}
+
+// ------------------------------------------------------------------------
+// numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
+// pairwise_sum_@TYPE@), applied by np.add.reduceat to a segment as
+// v[0] + pairwise(v[1:]).  `get(k)` returns the k-th value of the run.
+// Leaves: n < 8 sequential from -0.0; n <= 128 eight accumulators, a fixed
+// tree, then the tail.
+template <class T, class Get>
+__device__ T pw_leaf(Get get, long long off, long long n) {
+  if (n < 8) {
+    T r = T(-0.0);
+    for (long long i = 0; i < n; i++) r = r + get(off + i);
+    return r;
+  }
+  T r[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) r[j] = get(off + j);
+  long long i;
+  for (i = 8; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = r[j] + get(off + i + j);
+  }
+  T res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; i++) res = res + get(off + i);
+  return res;
+}
+
+// n > 128 splits at n2 = n/2 rounded down to a multiple of 8 and returns
+// sum(left) + sum(right).  Evaluated post-order with an explicit stack
+// (depth <= 26 for n < 2^32) -- no device recursion.
+template <class T, class Get>
+__device__ T pw_sum(Get get, long long off, long long n) {
+  if (n <= 128) return pw_leaf<T>(get, off, n);
+  long long s_off[32], s_n[32];
+  T s_left[32];
+  unsigned char s_stage[32];
+  int sp = 1;
+  s_off[0] = off;
+  s_n[0] = n;
+  s_stage[0] = 0;
+  T ret = T(0);
+  bool have = false;
+  while (true) {
+    if (!have) {
+      const int top = sp - 1;
+      if (s_n[top] <= 128) {
+        ret = pw_leaf<T>(get, s_off[top], s_n[top]);
+        have = true;
+        sp--;
+      } else {
+        long long n2 = s_n[top] / 2;
+        n2 -= n2 % 8;
+        s_stage[top] = 0;
+        s_off[sp] = s_off[top];
+        s_n[sp] = n2;
+        s_stage[sp] = 0;
+        sp++;
+      }
+    } else {
+      if (sp == 0) return ret;
+      const int top = sp - 1;
+      long long n2 = s_n[top] / 2;
+      n2 -= n2 % 8;
+      if (s_stage[top] == 0) {
+        s_left[top] = ret;
+        s_stage[top] = 1;
+        have = false;
+        s_off[sp] = s_off[top] + n2;
+        s_n[sp] = s_n[top] - n2;
+        s_stage[sp] = 0;
+        sp++;
+      } else {
+        ret = s_left[top] + ret;
+        sp--;
+      }
+    }
+  }
+}
+
+template <class T, class Get>
+__device__ T reduce_run(Get get, long long n, int mode) {
+  if (mode == kLast) return get(n - 1);
+  T v0 = get(0);
+  if (n == 1) return v0;
+  if (mode == kSumSeq) {
+    T acc = v0;
+    for (long long i = 1; i < n; i++) acc = acc + get(i);
+    return acc;
+  }
+  return v0 + pw_sum<T>(get, 1, n - 1);
+}
+
+// ------------------------------------------------------------------------
+template <class T>
+AS_DEVICE_INLINE long long lower_bound_dev(const T* a, long long n, T x) {
+  long long lo = 0, hi = n;
+  while (lo < hi) {
+    long long mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+template <class T>
+AS_DEVICE_INLINE long long upper_bound_dev(const T* a, long long n, T x) {
+  long long lo = 0, hi = n;
+  while (lo < hi) {
+    long long mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+AS_DEVICE_INLINE unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace as

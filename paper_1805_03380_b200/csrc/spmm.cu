@@ -1,0 +1,233 @@
+// spmm.cu -- sparse x dense products over the CSR (= cached transpose) of A.
+//
+//   C = A @ B, B column-major (n_cols x k), C column-major (n_rows x k).
+// Reference: _kernels.mat_times_vec (_kernels.py:118-127) is the k = 1 case;
+// SURVEY 3.3 defines k > 1 as k independent calls.  _kernels.vec_times_mat
+// (_kernels.py:106-115) is the row-vector product over the CSC itself.
+//
+// B200 design (row split, dense operand chunked to stay L2-resident):
+//  * the k dense columns are processed in chunks of KC (16 f32 / 8 f64 = 64 B
+//    per row); each chunk of B is first transposed into a row-major scratch
+//    Bt[n_cols][KC] (coalesced column reads, 64-byte row writes) that stays
+//    resident in the 126 MB L2 while A streams past it;
+//  * one thread per output row walks its CSR row in column order and gathers
+//    whole 64-byte Bt rows with 128-bit loads, so every L2 sector fetched is
+//    fully used;
+//  * the C chunk is written column by column, 32 consecutive rows per warp
+//    store (128-byte coalesced).
+// Exact mode mirrors the reference's arithmetic: float64 accumulator, product
+// and sum separately rounded, columns with B[j,c] == 0 skipped, contributions
+// in ascending column order -- bit-identical to mat_times_vec for float64.
+#include "capi_util.cuh"
+#include "common.cuh"
+
+namespace as {
+
+constexpr int kMmThreads = 256;
+
+template <class T, int KC>
+__global__ void __launch_bounds__(kMmThreads)
+dense_chunk_transpose_kernel(long long n, const T* __restrict__ B, long long ldb, int kc, T* __restrict__ Bt) {
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  T v[KC];
+#pragma unroll
+  for (int c = 0; c < KC; c++) v[c] = c < kc ? __ldcs(&B[j + (long long)c * ldb]) : T(0);
+  T* dst = Bt + j * KC;
+  constexpr int kVec = 16 / sizeof(T);
+#pragma unroll
+  for (int c = 0; c < KC; c += kVec) {
+    if constexpr (sizeof(T) == 4) {
+      float4 q = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+      *reinterpret_cast<float4*>(dst + c) = q;
+    } else {
+      double2 q = make_double2(v[c], v[c + 1]);
+      *reinterpret_cast<double2*>(dst + c) = q;
+    }
+  }
+}
+
+AS_DEVICE_INLINE float fma_t(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+AS_DEVICE_INLINE double fma_t(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+template <class T>
+AS_DEVICE_INLINE void load_row16B(const T* p, T* out);
+
+template <>
+AS_DEVICE_INLINE void load_row16B<float>(const float* p, float* out) {
+  float4 q = __ldg(reinterpret_cast<const float4*>(p));
+  out[0] = q.x;
+  out[1] = q.y;
+  out[2] = q.z;
+  out[3] = q.w;
+}
+template <>
+AS_DEVICE_INLINE void load_row16B<double>(const double* p, double* out) {
+  double2 q = __ldg(reinterpret_cast<const double2*>(p));
+  out[0] = q.x;
+  out[1] = q.y;
+}
+
+// one thread per output row; KC dense columns from the row-major chunk Bt
+template <class T, int KC, bool kExact>
+__global__ void __launch_bounds__(kMmThreads)
+spmm_rows_kernel(long long n_rows, const int* __restrict__ row_ptr, const int* __restrict__ col_idx,
+                 const T* __restrict__ vals, const T* __restrict__ Bt, int kc, T* __restrict__ C, long long ldc) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  using Acc = typename std::conditional<kExact, double, T>::type;
+  Acc acc[KC];
+#pragma unroll
+  for (int c = 0; c < KC; c++) acc[c] = Acc(0);
+  const int beg = row_ptr[r], end = row_ptr[r + 1];
+  constexpr int kVec = 16 / sizeof(T);
+  int k = beg;
+  for (; k + 1 < end; k += 2) {  // two entries in flight
+    const int j0 = __ldcs(&col_idx[k]), j1 = __ldcs(&col_idx[k + 1]);
+    const T v0 = __ldcs(&vals[k]), v1 = __ldcs(&vals[k + 1]);
+    T b0[KC], b1[KC];
+#pragma unroll
+    for (int c = 0; c < KC; c += kVec) {
+      load_row16B<T>(Bt + (long long)j0 * KC + c, b0 + c);
+      load_row16B<T>(Bt + (long long)j1 * KC + c, b1 + c);
+    }
+#pragma unroll
+    for (int c = 0; c < KC; c++) {
+      if (kExact) {
+        if (b0[c] != T(0)) acc[c] = __dadd_rn(acc[c], __dmul_rn((double)v0, (double)b0[c]));
+        if (b1[c] != T(0)) acc[c] = __dadd_rn(acc[c], __dmul_rn((double)v1, (double)b1[c]));
+      } else {
+        acc[c] = fma_t(v0, b0[c], acc[c]);
+        acc[c] = fma_t(v1, b1[c], acc[c]);
+      }
+    }
+  }
+  if (k < end) {
+    const int j0 = __ldcs(&col_idx[k]);
+    const T v0 = __ldcs(&vals[k]);
+    T b0[KC];
+#pragma unroll
+    for (int c = 0; c < KC; c += kVec) load_row16B<T>(Bt + (long long)j0 * KC + c, b0 + c);
+#pragma unroll
+    for (int c = 0; c < KC; c++) {
+      if (kExact) {
+        if (b0[c] != T(0)) acc[c] = __dadd_rn(acc[c], __dmul_rn((double)v0, (double)b0[c]));
+      } else {
+        acc[c] = fma_t(v0, b0[c], acc[c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < KC; c++)
+    if (c < kc) __stcs(&C[r + (long long)c * ldc], (T)acc[c]);
+}
+
+// k == 1 exact: y = A x as a per-row left fold (mat_times_vec, bit-exact)
+template <class T>
+__global__ void __launch_bounds__(kMmThreads)
+spmv_rows_exact_kernel(long long n_rows, const int* __restrict__ row_ptr, const int* __restrict__ col_idx,
+                       const T* __restrict__ vals, const T* __restrict__ x, T* __restrict__ y) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  double acc = 0.0;
+  const int beg = row_ptr[r], end = row_ptr[r + 1];
+  for (int k = beg; k < end; k++) {
+    const double xj = (double)__ldg(&x[col_idx[k]]);
+    if (xj != 0.0) acc = __dadd_rn(acc, __dmul_rn((double)vals[k], xj));
+  }
+  y[r] = (T)acc;
+}
+
+// w = v^T A over the CSC: w[j] = left fold of v[row] * val in column order
+// (_kernels.vec_times_mat, _kernels.py:106-115); one warp per 32 columns,
+// one thread per column.
+__global__ void __launch_bounds__(kMmThreads)
+vecmat_csc_kernel(long long n_cols, const int* __restrict__ col_ptr, const int* __restrict__ row_idx,
+                  const double* __restrict__ vals, const double* __restrict__ v, double* __restrict__ w) {
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_cols) return;
+  double s = 0.0;
+  for (int k = col_ptr[j]; k < col_ptr[j + 1]; k++) s = __dadd_rn(s, __dmul_rn(__ldg(&v[row_idx[k]]), vals[k]));
+  w[j] = s;
+}
+
+template <class T, int KC, bool kExact>
+static int spmm_impl(long long n_rows, long long n_cols, long long k, const int* row_ptr, const int* col_idx,
+                     const T* vals, const T* B, long long ldb, T* C, long long ldc, T* Bt, cudaStream_t st) {
+  const int blocks_r = (int)((n_rows + kMmThreads - 1) / kMmThreads);
+  const int blocks_c = (int)((n_cols + kMmThreads - 1) / kMmThreads);
+  for (long long k0 = 0; k0 < k; k0 += KC) {
+    const int kc = (int)min((long long)KC, k - k0);
+    if (n_cols > 0) {
+      dense_chunk_transpose_kernel<T, KC><<<blocks_c, kMmThreads, 0, st>>>(n_cols, B + k0 * ldb, ldb, kc, Bt);
+      AS_LAUNCH_CHECK();
+    }
+    if (n_rows > 0) {
+      spmm_rows_kernel<T, KC, kExact><<<blocks_r, kMmThreads, 0, st>>>(n_rows, row_ptr, col_idx, vals, Bt, kc,
+                                                                       C + k0 * ldc, ldc);
+      AS_LAUNCH_CHECK();
+    }
+  }
+  return AS_OK;
+}
+
+}  // namespace as
+
+using namespace as;
+
+extern "C" {
+
+size_t as_spmm_workspace_bytes(int64_t n_cols, int64_t k, int dtype_bytes) {
+  // one row-major chunk of B: n_cols x 64 bytes
+  (void)k;
+  (void)dtype_bytes;
+  return (size_t)(n_cols > 0 ? n_cols : 1) * 64 + 256;
+}
+
+int as_spmm_csr_f32(int64_t n_rows, int64_t n_cols, int64_t k, const int32_t* row_ptr, const int32_t* col_idx,
+                    const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc, int exact, void* ws,
+                    size_t ws_bytes, void* stream) {
+  AS_REQUIRE(n_rows >= 0 && n_cols >= 0 && k >= 0, AS_ERR_SHAPE, "negative dimension");
+  AS_REQUIRE(ldb >= n_cols && ldc >= n_rows, AS_ERR_ARG, "leading dimension too small");
+  AS_REQUIRE(ws_bytes >= as_spmm_workspace_bytes(n_cols, k, 4), AS_ERR_ARG, "workspace too small");
+  cudaStream_t st = S(stream);
+  if (k == 1 && exact) {
+    if (n_rows > 0)
+      spmv_rows_exact_kernel<float><<<(unsigned)((n_rows + kMmThreads - 1) / kMmThreads), kMmThreads, 0, st>>>(
+          n_rows, row_ptr, col_idx, vals, B, C);
+    AS_LAUNCH_CHECK();
+    return AS_OK;
+  }
+  if (exact) return spmm_impl<float, 16, true>(n_rows, n_cols, k, row_ptr, col_idx, vals, B, ldb, C, ldc, (float*)ws, st);
+  return spmm_impl<float, 16, false>(n_rows, n_cols, k, row_ptr, col_idx, vals, B, ldb, C, ldc, (float*)ws, st);
+}
+
+int as_spmm_csr_f64(int64_t n_rows, int64_t n_cols, int64_t k, const int32_t* row_ptr, const int32_t* col_idx,
+                    const double* vals, const double* B, int64_t ldb, double* C, int64_t ldc, void* ws,
+                    size_t ws_bytes, void* stream) {
+  AS_REQUIRE(n_rows >= 0 && n_cols >= 0 && k >= 0, AS_ERR_SHAPE, "negative dimension");
+  AS_REQUIRE(ldb >= n_cols && ldc >= n_rows, AS_ERR_ARG, "leading dimension too small");
+  AS_REQUIRE(ws_bytes >= as_spmm_workspace_bytes(n_cols, k, 8), AS_ERR_ARG, "workspace too small");
+  cudaStream_t st = S(stream);
+  if (k == 1) {
+    if (n_rows > 0)
+      spmv_rows_exact_kernel<double><<<(unsigned)((n_rows + kMmThreads - 1) / kMmThreads), kMmThreads, 0, st>>>(
+          n_rows, row_ptr, col_idx, vals, B, C);
+    AS_LAUNCH_CHECK();
+    return AS_OK;
+  }
+  return spmm_impl<double, 8, true>(n_rows, n_cols, k, row_ptr, col_idx, vals, B, ldb, C, ldc, (double*)ws, st);
+}
+
+int as_vecmat_csc_f64(int64_t n_rows, int64_t n_cols, const int32_t* col_ptr, const int32_t* row_idx,
+                      const double* vals, const double* v, double* w, void* stream) {
+  AS_REQUIRE(n_rows >= 0 && n_cols >= 0, AS_ERR_SHAPE, "negative dimension");
+  if (n_cols > 0) {
+    vecmat_csc_kernel<<<(unsigned)((n_cols + kMmThreads - 1) / kMmThreads), kMmThreads, 0, S(stream)>>>(
+        n_cols, col_ptr, row_idx, vals, v, w);
+    AS_LAUNCH_CHECK();
+  }
+  return AS_OK;
+}
+
+}  // extern "C"
