@@ -1,0 +1,292 @@
+"""Compressed Sparse Column storage, resident on the GPU.
+
+Mirrors autosparse/csc.py (Dims, Triplet, CscData, canonicalize,
+from_triplets, empty, check_coords, validate; csc.py:24-222, 363-383) with
+the arrays in HBM: col_ptr int32[n_cols+1], row_idx int32[nnz], vals
+float64 (float32 allowed as an extension).  The reference-typed views
+(`values` float64, `row_indices` / `col_offsets` int64, numpy) are
+materialised on first access and cached; element-level reads use that host
+mirror, bulk work runs on the device.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Iterator, NamedTuple, Sequence
+
+import numpy as np
+import torch
+
+from . import _kernels
+from .errors import CoordinateError, CorruptionError
+
+INDEX_MAX = np.iinfo(np.int64).max
+DEVICE_INDEX_MAX = np.iinfo(np.int32).max
+
+DUP_SUM = "sum"
+DUP_LAST = "last"
+
+
+def default_device():
+    return torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
+
+
+@dataclass(frozen=True)
+class Dims:
+    """Matrix shape (csc.py:24-45).  Either dimension may be zero."""
+
+    n_rows: int
+    n_cols: int
+
+    def __post_init__(self):
+        if self.n_rows < 0 or self.n_cols < 0:
+            raise ValueError("dimensions must be non-negative, got %r" % (self,))
+        if self.n_rows and self.n_cols > INDEX_MAX // self.n_rows:
+            raise ValueError("n_rows * n_cols overflows the 64-bit index type")
+
+    @property
+    def n_cells(self) -> int:
+        return self.n_rows * self.n_cols
+
+    def __iter__(self):
+        return iter((self.n_rows, self.n_cols))
+
+    def __str__(self):
+        return "%dx%d" % (self.n_rows, self.n_cols)
+
+
+class Triplet(NamedTuple):
+    row: int
+    col: int
+    value: float
+
+
+def _to_dev(a, dtype, device):
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=dtype, non_blocking=True).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(device, non_blocking=True)
+
+
+class CscData:
+    """Canonical CSC matrix (sorted, duplicate-free, zero-free) in HBM."""
+
+    __slots__ = ("dims", "col_ptr", "row_idx", "vals", "_host")
+
+    def __init__(self, dims: Dims, col_ptr, row_idx, vals, device=None):
+        if dims.n_rows > DEVICE_INDEX_MAX or dims.n_cols > DEVICE_INDEX_MAX:
+            raise CoordinateError("%s exceeds the int32 device index range" % (dims,))
+        device = device or (col_ptr.device if isinstance(col_ptr, torch.Tensor) else default_device())
+        self.dims = dims
+        self.col_ptr = _to_dev(col_ptr, torch.int32, device)
+        self.row_idx = _to_dev(row_idx, torch.int32, device)
+        vdt = vals.dtype if isinstance(vals, torch.Tensor) and vals.dtype in (torch.float32, torch.float64) else torch.float64
+        self.vals = _to_dev(vals, vdt, device)
+        self._host = None
+
+    @classmethod
+    def from_reference_arrays(cls, dims: Dims, values, row_indices, col_offsets, device=None) -> "CscData":
+        """Wrap the reference's (values, row_indices, col_offsets) order."""
+        return cls(dims, col_offsets, row_indices, values, device=device)
+
+    # -- device view ----------------------------------------------------------
+    @property
+    def device(self):
+        return self.col_ptr.device
+
+    @property
+    def arrays(self):
+        """(col_ptr, row_idx, vals) device tensors, the kernels' operand order."""
+        return self.col_ptr, self.row_idx, self.vals
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_idx.shape[0])
+
+    # -- reference-typed host mirror (csc.py:54-67) -----------------------------
+    def _mirror(self):
+        if self._host is None:
+            self._host = (
+                self.vals.double().cpu().numpy(),
+                self.row_idx.cpu().numpy().astype(np.int64),
+                self.col_ptr.cpu().numpy().astype(np.int64),
+            )
+        return self._host
+
+    @property
+    def values(self) -> np.ndarray:
+        return self._mirror()[0]
+
+    @property
+    def row_indices(self) -> np.ndarray:
+        return self._mirror()[1]
+
+    @property
+    def col_offsets(self) -> np.ndarray:
+        return self._mirror()[2]
+
+    def find(self, row: int, col: int) -> int:
+        """Storage position of (row, col) or -1 (binary search in the column)."""
+        offs, rows = self.col_offsets, self.row_indices
+        start, end = offs[col], offs[col + 1]
+        pos = start + int(np.searchsorted(rows[start:end], row))
+        return pos if pos < end and rows[pos] == row else -1
+
+    def get(self, row: int, col: int) -> float:
+        check_coords(self.dims, row, col)
+        pos = self.find(row, col)
+        return float(self.values[pos]) if pos >= 0 else 0.0
+
+    def set_value_at(self, pos: int, value: float) -> None:
+        """In-place overwrite of a stored value (the only sanctioned mutation,
+        csc.py:57-58 / hybrid.py:170-178); device and mirror stay in sync."""
+        self.vals[pos] = value
+        if self._host is not None:
+            self._host[0][pos] = value
+
+    def col_count(self, col: int) -> int:
+        if not 0 <= col < self.dims.n_cols:
+            raise CoordinateError("column %d outside matrix with %d columns" % (col, self.dims.n_cols))
+        offs = self.col_offsets
+        return int(offs[col + 1] - offs[col])
+
+    def triplets(self) -> Iterator[Triplet]:
+        vals, rows, offs = self._mirror()
+        for col in range(self.dims.n_cols):
+            for k in range(offs[col], offs[col + 1]):
+                yield Triplet(int(rows[k]), col, float(vals[k]))
+
+    def expand_cols(self) -> np.ndarray:
+        return np.repeat(np.arange(self.dims.n_cols, dtype=np.int64), np.diff(self.col_offsets))
+
+    def expand_cols_device(self) -> torch.Tensor:
+        counts = (self.col_ptr[1:] - self.col_ptr[:-1]).long()
+        return torch.repeat_interleave(torch.arange(self.dims.n_cols, device=self.device, dtype=torch.int32), counts)
+
+    def to_dense(self) -> np.ndarray:
+        dense = np.zeros((self.dims.n_rows, self.dims.n_cols))
+        dense[self.row_indices, self.expand_cols()] = self.values
+        return dense
+
+    def copy(self) -> "CscData":
+        return CscData(self.dims, self.col_ptr.clone(), self.row_idx.clone(), self.vals.clone())
+
+    def same_elements(self, other: "CscData") -> bool:
+        return (
+            self.dims == other.dims
+            and self.nnz == other.nnz
+            and torch.equal(self.col_ptr, other.col_ptr.to(self.device))
+            and torch.equal(self.row_idx, other.row_idx.to(self.device))
+            and torch.equal(self.vals.double(), other.vals.double().to(self.device))
+        )
+
+    def __repr__(self):
+        return "<CscData %s nnz=%d on %s>" % (self.dims, self.nnz, self.device)
+
+
+def check_coords(dims: Dims, row: int, col: int) -> None:
+    if not (0 <= row < dims.n_rows and 0 <= col < dims.n_cols):
+        raise CoordinateError("coordinate (%d, %d) outside %s matrix" % (row, col, dims))
+
+
+def empty(dims: Dims, device=None, dtype=torch.float64) -> CscData:
+    device = device or default_device()
+    return CscData(dims, torch.zeros(dims.n_cols + 1, dtype=torch.int32, device=device),
+                   torch.empty(0, dtype=torch.int32, device=device), torch.empty(0, dtype=dtype, device=device))
+
+
+def _as_index_tensor(a, device):
+    if isinstance(a, torch.Tensor):
+        t = a.to(device, non_blocking=True)
+        return t if t.dtype in (torch.int32, torch.int64) else t.long()
+    arr = np.asarray(a)
+    if arr.dtype not in (np.int32, np.int64):
+        arr = arr.astype(np.int64)
+    return torch.as_tensor(np.ascontiguousarray(arr)).to(device, non_blocking=True)
+
+
+def _as_value_tensor(a, device, dtype=None):
+    if isinstance(a, torch.Tensor):
+        dt = dtype or (a.dtype if a.dtype in (torch.float32, torch.float64) else torch.float64)
+        return a.to(device=device, dtype=dt, non_blocking=True).contiguous()
+    arr = np.asarray(a, dtype=np.float64 if dtype in (None, torch.float64) else np.float32)
+    return torch.as_tensor(np.ascontiguousarray(arr)).to(device, non_blocking=True)
+
+
+def build_device(dims: Dims, rows, cols, values, dup: str = DUP_SUM, device=None):
+    """Run the GPU construction on device (or host) arrays; returns
+    (CscData, first_bad_index_or_None)."""
+    if dup not in (DUP_SUM, DUP_LAST):
+        raise ValueError("unknown duplicate policy %r" % (dup,))
+    device = device or default_device()
+    r = _as_index_tensor(rows, device)
+    c = _as_index_tensor(cols, device)
+    if r.dtype != c.dtype:
+        r, c = r.long(), c.long()
+    v = _as_value_tensor(values, device)
+    p, ri, vv, bad = _kernels.coo_to_csc(dims.n_rows, dims.n_cols, r, c, v, dup)
+    return CscData(dims, p, ri, vv), bad
+
+
+def canonicalize(dims: Dims, rows, cols, values, dup: str = DUP_SUM, device=None) -> CscData:
+    """Canonical CSC from parallel coordinate arrays (csc.py:148-193): stable
+    column-major order, duplicates per `dup`, exact zeros pruned -- one
+    sort/reduce/compact pass on the GPU."""
+    m, bad = build_device(dims, rows, cols, values, dup, device)
+    if bad is not None:
+        raise CoordinateError("coordinate %d outside %s matrix" % (bad, dims))
+    return m
+
+
+def _coords_from_triplets(triplets: Sequence) -> tuple:
+    """(rows, cols, values) from a reference-style triplet sequence
+    (csc.py:196-205), or passed through when given as three arrays."""
+    if isinstance(triplets, tuple) and len(triplets) == 3 and all(
+        isinstance(x, (np.ndarray, torch.Tensor)) for x in triplets
+    ):
+        return triplets
+    n = len(triplets)
+    if n == 0:
+        return np.empty(0, np.int64), np.empty(0, np.int64), np.empty(0, np.float64)
+    rows = np.fromiter((t[0] for t in triplets), dtype=np.int64, count=n)
+    cols = np.fromiter((t[1] for t in triplets), dtype=np.int64, count=n)
+    vals = np.fromiter((t[2] for t in triplets), dtype=np.float64, count=n)
+    return rows, cols, vals
+
+
+def from_triplets(dims: Dims, triplets, dup: str = DUP_SUM, device=None) -> CscData:
+    """Batch-build canonical CSC (csc.py:208-222).  `triplets` is a sequence
+    of (row, col, value) or, as an extension, a tuple of three arrays/tensors.
+    Out-of-range triplets raise CoordinateError naming the first one."""
+    rows, cols, vals = _coords_from_triplets(triplets)
+    m, bad = build_device(dims, rows, cols, vals, dup, device)
+    if bad is not None:
+        r = int(rows[bad])
+        c = int(cols[bad])
+        v = float(vals[bad])
+        raise CoordinateError("triplet %d = (%d, %d, %g) outside %s matrix" % (bad, r, c, v, dims))
+    return m
+
+
+def validate(m: CscData) -> None:
+    """Canonical-form checker (csc.py:363-383): raises CorruptionError."""
+    dims = m.dims
+    vals, rows, offs = m.values, m.row_indices, m.col_offsets
+    n = rows.shape[0]
+    if offs.shape[0] != dims.n_cols + 1:
+        raise CorruptionError("column offsets array has wrong length")
+    if offs[0] != 0 or offs[-1] != n:
+        raise CorruptionError("column offsets must start at 0 and end at nnz")
+    if (np.diff(offs) < 0).any():
+        raise CorruptionError("column offsets must be non-decreasing")
+    if vals.shape[0] != n:
+        raise CorruptionError("row index array length differs from value array")
+    if n:
+        if rows.min() < 0 or rows.max() >= dims.n_rows:
+            raise CorruptionError("row index outside matrix")
+        cols = m.expand_cols()
+        same_col = cols[1:] == cols[:-1]
+        if (same_col & (rows[1:] <= rows[:-1])).any():
+            bad = int(cols[1:][same_col & (rows[1:] <= rows[:-1])][0])
+            raise CorruptionError("rows in column %d not strictly increasing" % bad)
+        if (vals == 0.0).any():
+            raise CorruptionError("exact zero stored in values array")
