@@ -8,133 +8,188 @@
 //                 base CSC ++ write log, reduce = last, prune zeros (= erase)
 //   transpose     _kernels.transpose (_kernels.py:130-150): bucket = row,
 //                 minor = col (unique per bucket), no reduce, no prune
-// Kernel sequence per call (one stream, no host sync):
-//   memset -> count (warp-aggregated atomics) -> chained-scan of counts ->
-//   scatter (u64 keys) -> seg_tile_kernel (sort + reduce + chained compaction)
+// Each call is two memsets and ONE cooperative launch of
+// persist_bucket_kernel (persist.cuh); no host synchronisation.
 #include "capi_util.cuh"
-#include "segsort.cuh"
+#include "persist.cuh"
+
+#include <stdlib.h>
 
 namespace as {
 
-struct BuildWs {
-  unsigned* tickets;               // [0] scan, [1] seg engine
-  unsigned long long* scan_states;
-  unsigned long long* seg_states;
+constexpr long long kMaxDim = 0x7fffffffll;
+constexpr long long kMaxGrid = 148 * 8;  // upper bound of the co-resident grid
+constexpr long long kNprMax = 64;        // chunk ranges of the phase-2 work items
+
+struct PersistWs {
+  unsigned* zero;  // [0] ticket, [16] barrier arrive, [32] barrier generation
   unsigned* counts;
+  size_t zero_bytes;
+  unsigned* partials;
+  unsigned* range_sum;
+  long long* cta_sums;
   long long* seg_ptr;
+  long long* tile_c0;
+  long long* tile_total;
   unsigned long long* keys;
   unsigned long long* keys_alt;
-  char* zero_begin;
-  size_t zero_bytes;
+  void* vals_b;
+  int* tmp_rows;
+  void* tmp_vals;
+  long long n_tiles, P1;
+  int smem_hist;
 };
 
-static inline long long seg_tiles(long long n) { return seg_engine_tiles(n); }
-static inline long long scan_tiles(long long n) {
-  const long long per = (long long)kScanThreads * kScanItems;
-  return n > 0 ? (n + per - 1) / per : 1;
+// histogram chunks: one per CTA of the co-resident grid (<= 3 x 148) so the
+// histogram and scatter phases use every SM; >= 256 elements per chunk and
+// the partials matrix capped at 8M entries.
+static inline long long choose_p1(long long n, long long nb) {
+  if (nb <= 0) return 1;
+  long long p = std::min(444ll, std::max(1ll, n / 256));
+  p = std::min(p, std::max(1ll, (8ll << 20) / nb));
+  return p;
 }
 
-static size_t carve_build(Carve& c, BuildWs* w, long long n, long long n_seg) {
-  w->tickets = c.take<unsigned>(64);
-  w->scan_states = c.take<unsigned long long>(scan_tiles(n_seg));
-  w->seg_states = c.take<unsigned long long>(seg_tiles(n));
-  w->counts = c.take<unsigned>(n_seg > 0 ? n_seg : 1);
-  w->zero_begin = (char*)w->tickets;
+static size_t carve_persist(Carve& c, PersistWs* w, long long n, long long nb, size_t val_bytes) {
+  w->n_tiles = seg_engine_tiles(n);
+  w->smem_hist = (nb <= kHistMaxBins && n >= nb) ? 1 : 0;
+  w->P1 = w->smem_hist ? choose_p1(n, nb) : 1;
+  w->zero = c.take<unsigned>(64);
+  w->counts = c.take<unsigned>(w->smem_hist ? 1 : std::max(1ll, nb));
   w->zero_bytes = c.off;
-  w->seg_ptr = c.take<long long>(n_seg + 1);
-  w->keys = c.take<unsigned long long>(n > 0 ? n : 1);
-  w->keys_alt = c.take<unsigned long long>(n > 0 ? n : 1);
+  w->partials = c.take<unsigned>(w->smem_hist ? w->P1 * nb : 1);
+  w->range_sum = c.take<unsigned>(w->smem_hist ? kNprMax * nb : 1);
+  w->cta_sums = c.take<long long>(2 * kMaxGrid);
+  w->seg_ptr = c.take<long long>(nb + 1);
+  w->tile_c0 = c.take<long long>(w->n_tiles + 1);
+  w->tile_total = c.take<long long>(w->n_tiles);
+  const long long n1 = std::max(1ll, n);
+  w->keys = c.take<unsigned long long>(n1);
+  w->keys_alt = c.take<unsigned long long>(n1);
+  w->vals_b = (void*)c.take<char>(n1 * val_bytes);
+  w->tmp_rows = c.take<int>(n1);
+  w->tmp_vals = (void*)c.take<char>(n1 * val_bytes);
+  c.take<long long>(2);
   return c.off;
 }
 
-template <class T>
-static int run_seg_engine(const BuildWs& w, long long n_seg, long long n_upper, int row_bits, int idx_bits,
-                          int presorted, ValSrc<T> vs, int mode, int prune, int* col_ptr, int* row_idx,
-                          T* vals, long long* info, cudaStream_t st) {
-  return launch_seg_engine<T>(w.seg_ptr, n_seg, n_upper, w.keys, w.keys_alt, row_bits, idx_bits, presorted, vs, mode,
-                              prune, col_ptr, row_idx, vals, info, w.seg_states, w.tickets + 1, st);
-}
-
-static int run_scan(const BuildWs& w, long long n_seg, cudaStream_t st) {
-  count_scan_kernel<<<(unsigned)scan_tiles(n_seg), kScanThreads, 0, st>>>(w.counts, n_seg, w.seg_ptr,
-                                                                          w.scan_states, w.tickets);
-  AS_LAUNCH_CHECK();
+template <class T, class S1, class S2>
+static int launch_persist(PersistArgs<T, S1, S2>& a, cudaStream_t st) {
+  static int grid = 0;
+  const size_t smem = sizeof(PersistSmem<T>);
+  auto kern = persist_bucket_kernel<T, S1, S2>;
+  if (grid == 0) {
+    AS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0, dev = 0, sms = 0;
+    AS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSegThreads, smem));
+    AS_CUDA_TRY(cudaGetDevice(&dev));
+    AS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    AS_REQUIRE(per_sm > 0, AS_ERR_CUDA, "persistent kernel does not fit on an SM");
+    grid = (int)std::min<long long>((long long)per_sm * sms, kMaxGrid);
+  }
+  void* args[] = {(void*)&a};
+  AS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSegThreads), args, smem, st));
   return AS_OK;
 }
 
-#define AS_TRY(expr)             \
-  do {                           \
-    int _rc = (expr);            \
-    if (_rc != AS_OK) return _rc; \
-  } while (0)
+template <class T, class S1, class S2>
+static int run_persist(const S1& s1, const S2& s2, long long nb, int row_bits, int mode, int prune, ValSrc<T> vs,
+                       int* col_ptr, int* row_idx, T* out_vals, long long* info, bool init_info, void* ws,
+                       size_t ws_bytes, cudaStream_t st) {
+  const long long n = s1.size() + s2.size();
+  Carve c(ws, ws_bytes);
+  PersistWs w;
+  carve_persist(c, &w, n, nb, sizeof(T));
+  long long* own_info = (long long*)(c.base ? c.base + c.off - 256 : nullptr);
+  AS_REQUIRE(c.ok, AS_ERR_ARG, "workspace too small: %zu < %zu", ws_bytes, c.off);
+  if (info == nullptr) info = own_info;
+  AS_CUDA_TRY(cudaMemsetAsync(w.zero, 0, w.zero_bytes, st));
+  if (init_info) AS_CUDA_TRY(cudaMemsetAsync(info, 0x7f, 2 * sizeof(long long), st));
+  PersistArgs<T, S1, S2> a;
+  a.s1 = s1;
+  a.s2 = s2;
+  a.n_bins = nb;
+  a.n_upper = n;
+  a.P1 = w.P1;
+  a.smem_hist = w.smem_hist;
+  a.partials = w.partials;
+  a.counts = w.counts;
+  a.range_sum = w.range_sum;
+  a.n_pr_max = kNprMax;
+  a.cta_sums = w.cta_sums;
+  a.seg_ptr = w.seg_ptr;
+  a.tile_c0 = w.tile_c0;
+  a.n_tiles = w.n_tiles;
+  a.tile_total = w.tile_total;
+  a.keys = w.keys;
+  a.keys_alt = w.keys_alt;
+  a.vals_b = (T*)w.vals_b;
+  a.tmp_rows = w.tmp_rows;
+  a.tmp_vals = (T*)w.tmp_vals;
+  a.row_bits = row_bits;
+  a.idx_bits = bits_for(n > 0 ? n - 1 : 0);
+  a.mode = mode;
+  a.prune = prune;
+  a.vs = vs;
+  a.col_ptr = col_ptr;
+  a.row_idx = row_idx;
+  a.out_vals = out_vals;
+  a.info = info;
+  a.ticket = w.zero;
+  a.gb = GridBar{w.zero + 16, w.zero + 32};
+  a.phase_ts = nullptr;
+  static unsigned long long* dbg_ts = nullptr;
+  const bool phase_dbg = getenv("AS_PHASE_TIMES") != nullptr;
+  if (phase_dbg) {
+    if (!dbg_ts) AS_CUDA_TRY(cudaMalloc(&dbg_ts, 16 * sizeof(unsigned long long)));
+    AS_CUDA_TRY(cudaMemsetAsync(dbg_ts, 0, 16 * sizeof(unsigned long long), st));
+    a.phase_ts = dbg_ts;
+  }
+  const int rc = launch_persist<T, S1, S2>(a, st);
+  if (phase_dbg && rc == AS_OK) {
+    unsigned long long h[16];
+    AS_CUDA_TRY(cudaMemcpyAsync(h, dbg_ts, sizeof(h), cudaMemcpyDeviceToHost, st));
+    AS_CUDA_TRY(cudaStreamSynchronize(st));
+    fprintf(stderr, "[phases n=%lld nb=%lld smem_hist=%d P1=%lld]", n, nb, w.smem_hist, w.P1);
+    for (int i = 1; i < 16 && h[i]; i++) fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
+    fprintf(stderr, " us\n");
+  }
+  return rc;
+}
 
-constexpr long long kMaxDim = 0x7fffffffll;
+size_t persist_ws_bytes(long long n, long long nb, size_t val_bytes) {
+  Carve c(nullptr, 0);
+  PersistWs w;
+  carve_persist(c, &w, n, nb, val_bytes);
+  return c.off;
+}
 
 template <class T, class IdxT>
 static int coo_to_csc(long long n_rows, long long n_cols, long long n, const IdxT* rows, const IdxT* cols,
-                      const T* vals, int dup, int* col_ptr, int* row_idx, T* out_vals, long long* info,
-                      void* ws, size_t ws_bytes, cudaStream_t st) {
+                      const T* vals, int dup, int* col_ptr, int* row_idx, T* out_vals, long long* info, void* ws,
+                      size_t ws_bytes, cudaStream_t st) {
   AS_REQUIRE(n_rows >= 0 && n_cols >= 0 && n_rows <= kMaxDim && n_cols <= kMaxDim, AS_ERR_SHAPE,
              "dimensions %lldx%lld outside the int32 device index range", n_rows, n_cols);
   AS_REQUIRE(n >= 0 && n <= kMaxDim, AS_ERR_ARG, "triplet count %lld outside the int32 range", n);
   AS_REQUIRE(dup == AS_DUP_SUM || dup == AS_DUP_LAST, AS_ERR_ARG, "unknown duplicate policy %d", dup);
-  Carve c(ws, ws_bytes);
-  BuildWs w;
-  carve_build(c, &w, n, n_cols);
-  AS_REQUIRE(c.ok, AS_ERR_ARG, "workspace too small: %zu < %zu", ws_bytes, c.off);
-  AS_CUDA_TRY(cudaMemsetAsync(w.zero_begin, 0, w.zero_bytes, st));
-  AS_CUDA_TRY(cudaMemsetAsync(info, 0x7f, 2 * sizeof(long long), st));
-  const int B = 256;
-  if (n > 0) {
-    coo_count_kernel<IdxT><<<grid_for(n, B), B, 0, st>>>(n, rows, cols, n_rows, n_cols, w.counts, info + 1);
-    AS_LAUNCH_CHECK();
-  }
-  AS_TRY(run_scan(w, n_cols, st));
-  if (n > 0) {
-    coo_scatter_kernel<IdxT><<<grid_for(n, B), B, 0, st>>>(n, rows, cols, n_rows, n_cols, w.seg_ptr, w.counts,
-                                                           w.keys, 0ull);
-    AS_LAUNCH_CHECK();
-  }
+  CooSrc<IdxT, T> s1{rows, cols, vals, n, n_rows, n_cols, 0ull, info + 1};
   ValSrc<T> vs{vals, nullptr, (unsigned long long)n};
-  return run_seg_engine<T>(w, n_cols, n, bits_for(n_rows > 0 ? n_rows - 1 : 0), bits_for(n > 0 ? n - 1 : 0), 0,
-                           vs, dup == AS_DUP_SUM ? kSumPairwise : kLast, 1, col_ptr, row_idx, out_vals, info, st);
+  return run_persist<T>(s1, NoSrc<T>{}, n_cols, bits_for(n_rows > 0 ? n_rows - 1 : 0),
+                        dup == AS_DUP_SUM ? kSumPairwise : kLast, 1, vs, col_ptr, row_idx, out_vals, info, true, ws,
+                        ws_bytes, st);
 }
 
 template <class T>
-static int csc_transpose(long long n_rows, long long n_cols, long long nnz, const int* col_ptr,
-                         const int* row_idx, const T* vals, int* t_col_ptr, int* t_row_idx, T* t_vals,
-                         void* ws, size_t ws_bytes, cudaStream_t st) {
+static int csc_transpose(long long n_rows, long long n_cols, long long nnz, const int* col_ptr, const int* row_idx,
+                         const T* vals, int* t_col_ptr, int* t_row_idx, T* t_vals, void* ws, size_t ws_bytes,
+                         cudaStream_t st) {
   AS_REQUIRE(n_rows >= 0 && n_cols >= 0 && n_rows <= kMaxDim && n_cols <= kMaxDim, AS_ERR_SHAPE,
              "dimensions %lldx%lld outside the int32 device index range", n_rows, n_cols);
   AS_REQUIRE(nnz >= 0 && nnz <= kMaxDim, AS_ERR_ARG, "nnz %lld outside the int32 range", nnz);
-  Carve c(ws, ws_bytes);
-  BuildWs w;
-  carve_build(c, &w, nnz, n_rows);
-  long long* info = c.take<long long>(2);
-  AS_REQUIRE(c.ok, AS_ERR_ARG, "workspace too small: %zu < %zu", ws_bytes, c.off);
-  AS_CUDA_TRY(cudaMemsetAsync(w.zero_begin, 0, w.zero_bytes, st));
-  const int B = 256;
-  if (nnz > 0) {
-    row_count_kernel<<<grid_for(nnz, B), B, 0, st>>>(nnz, row_idx, w.counts);
-    AS_LAUNCH_CHECK();
-  }
-  AS_TRY(run_scan(w, n_rows, st));
-  if (nnz > 0) {
-    csc_scatter_kernel<true><<<grid_for(nnz, B), B, 0, st>>>(n_cols, nnz, col_ptr, row_idx, w.seg_ptr, w.counts,
-                                                             w.keys);
-    AS_LAUNCH_CHECK();
-  }
+  CscSrc<T> s1{col_ptr, row_idx, vals, n_cols, nnz, true, 0ull};
   ValSrc<T> vs{vals, nullptr, (unsigned long long)nnz};
-  return run_seg_engine<T>(w, n_rows, nnz, bits_for(n_cols > 0 ? n_cols - 1 : 0), bits_for(nnz > 0 ? nnz - 1 : 0),
-                           0, vs, kLast, 0, t_col_ptr, t_row_idx, t_vals, info, st);
-}
-
-size_t build_ws_bytes(long long n, long long n_seg) {
-  Carve c(nullptr, 0);
-  BuildWs w;
-  carve_build(c, &w, n, n_seg);
-  c.take<long long>(2);
-  return c.off;
+  return run_persist<T>(s1, NoSrc<T>{}, n_rows, bits_for(n_cols > 0 ? n_cols - 1 : 0), kLast, 0, vs, t_col_ptr,
+                        t_row_idx, t_vals, nullptr, false, ws, ws_bytes, st);
 }
 
 }  // namespace as
@@ -143,11 +198,11 @@ using namespace as;
 
 extern "C" {
 
-size_t as_build_workspace_bytes(int64_t n, int64_t n_cols) { return build_ws_bytes(n, n_cols); }
+size_t as_build_workspace_bytes(int64_t n, int64_t n_cols) { return persist_ws_bytes(n, n_cols, 8); }
 size_t as_flush_workspace_bytes(int64_t nnz_base, int64_t n_log, int64_t n_cols) {
-  return build_ws_bytes(nnz_base + n_log, n_cols);
+  return persist_ws_bytes(nnz_base + n_log, n_cols, 8);
 }
-size_t as_transpose_workspace_bytes(int64_t nnz, int64_t n_rows) { return build_ws_bytes(nnz, n_rows); }
+size_t as_transpose_workspace_bytes(int64_t nnz, int64_t n_rows) { return persist_ws_bytes(nnz, n_rows, 8); }
 
 #define AS_BUILD_DISPATCH(T)                                                                                    \
   if (idx_bytes == 4)                                                                                            \
@@ -175,41 +230,16 @@ int as_flush_log_f64(int64_t n_rows, int64_t n_cols, int64_t nnz_base, const int
                      const int32_t* base_row_idx, const double* base_vals, int64_t n_log, const int32_t* log_rows,
                      const int32_t* log_cols, const double* log_vals, int32_t* col_ptr, int32_t* row_idx,
                      double* out_vals, int64_t* info, void* ws, size_t ws_bytes, void* stream) {
-  cudaStream_t st = S(stream);
   AS_REQUIRE(n_rows >= 0 && n_cols >= 0 && n_rows <= kMaxDim && n_cols <= kMaxDim, AS_ERR_SHAPE,
              "dimensions %lldx%lld outside the int32 device index range", (long long)n_rows, (long long)n_cols);
-  const long long n = nnz_base + n_log;
-  AS_REQUIRE(nnz_base >= 0 && n_log >= 0 && n <= kMaxDim, AS_ERR_ARG, "element count outside the int32 range");
-  Carve c(ws, ws_bytes);
-  BuildWs w;
-  carve_build(c, &w, n, n_cols);
-  AS_REQUIRE(c.ok, AS_ERR_ARG, "workspace too small: %zu < %zu", ws_bytes, c.off);
-  AS_CUDA_TRY(cudaMemsetAsync(w.zero_begin, 0, w.zero_bytes, st));
-  AS_CUDA_TRY(cudaMemsetAsync(info, 0x7f, 2 * sizeof(long long), st));
-  const int B = 256;
-  if (nnz_base > 0) {
-    csc_count_kernel<<<grid_for(n_cols, B), B, 0, st>>>(n_cols, base_col_ptr, w.counts);
-    AS_LAUNCH_CHECK();
-  }
-  if (n_log > 0) {
-    coo_count_kernel<int><<<grid_for(n_log, B), B, 0, st>>>(n_log, log_rows, log_cols, n_rows, n_cols, w.counts,
-                                                             (long long*)info + 1);
-    AS_LAUNCH_CHECK();
-  }
-  AS_TRY(run_scan(w, n_cols, st));
-  if (nnz_base > 0) {
-    csc_scatter_kernel<false><<<grid_for(nnz_base, B), B, 0, st>>>(n_cols, nnz_base, base_col_ptr, base_row_idx,
-                                                                   w.seg_ptr, w.counts, w.keys);
-    AS_LAUNCH_CHECK();
-  }
-  if (n_log > 0) {
-    coo_scatter_kernel<int><<<grid_for(n_log, B), B, 0, st>>>(n_log, log_rows, log_cols, n_rows, n_cols, w.seg_ptr,
-                                                              w.counts, w.keys, (unsigned long long)nnz_base);
-    AS_LAUNCH_CHECK();
-  }
+  AS_REQUIRE(nnz_base >= 0 && n_log >= 0 && nnz_base + n_log <= kMaxDim, AS_ERR_ARG,
+             "element count outside the int32 range");
+  CscSrc<double> s1{base_col_ptr, base_row_idx, base_vals, n_cols, nnz_base, false, 0ull};
+  CooSrc<int, double> s2{log_rows, log_cols, log_vals, n_log, n_rows, n_cols, (unsigned long long)nnz_base,
+                         (long long*)info + 1};
   ValSrc<double> vs{base_vals, log_vals, (unsigned long long)nnz_base};
-  return run_seg_engine<double>(w, n_cols, n, bits_for(n_rows > 0 ? n_rows - 1 : 0), bits_for(n > 0 ? n - 1 : 0), 0,
-                                vs, kLast, 1, col_ptr, row_idx, out_vals, (long long*)info, st);
+  return run_persist<double>(s1, s2, n_cols, bits_for(n_rows > 0 ? n_rows - 1 : 0), kLast, 1, vs, col_ptr, row_idx,
+                             out_vals, (long long*)info, true, ws, ws_bytes, S(stream));
 }
 
 int as_csc_transpose_f64(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* col_ptr, const int32_t* row_idx,

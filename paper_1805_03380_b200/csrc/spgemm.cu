@@ -126,7 +126,8 @@ int as_spgemm_products(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, cons
                                                                                    b_row_idx, counts);
     AS_LAUNCH_CHECK();
   }
-  count_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(counts, n_cols_b, (long long*)prod_ptr, states, ticket);
+  count_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(counts, n_cols_b, (long long*)prod_ptr, states, ticket,
+                                                              nullptr, 0);
   AS_LAUNCH_CHECK();
   AS_CUDA_TRY(cudaMemcpyAsync(info, prod_ptr + n_cols_b, sizeof(long long), cudaMemcpyDeviceToDevice, st));
   return AS_OK;
@@ -137,6 +138,7 @@ size_t as_spgemm_workspace_bytes(int64_t n_cols_b, int64_t total_products) {
   Carve c(nullptr, 0);
   c.take<unsigned>(64);
   c.take<unsigned long long>(seg_engine_tiles(total_products));
+  c.take<long long>(seg_engine_tiles(total_products) + 1);
   c.take<unsigned long long>(total_products > 0 ? total_products : 1);
   c.take<unsigned long long>(total_products > 0 ? total_products : 1);
   c.take<double>(total_products > 0 ? total_products : 1);
@@ -157,6 +159,8 @@ int as_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int
   unsigned* ticket = c.take<unsigned>(64);
   unsigned long long* states = c.take<unsigned long long>(seg_engine_tiles(total_products));
   const size_t zero_bytes = c.off;
+  const long long n_tiles = seg_engine_tiles(total_products);
+  long long* tile_c0 = c.take<long long>(n_tiles + 1);
   unsigned long long* keys = c.take<unsigned long long>(total_products > 0 ? total_products : 1);
   unsigned long long* keys_alt = c.take<unsigned long long>(total_products > 0 ? total_products : 1);
   double* pvals = c.take<double>(total_products > 0 ? total_products : 1);
@@ -166,8 +170,10 @@ int as_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int
         n_cols_b, a_col_ptr, a_row_idx, a_vals, b_col_ptr, b_row_idx, b_vals, (const long long*)prod_ptr, keys, pvals);
     AS_LAUNCH_CHECK();
   }
+  tile_bounds_kernel<<<grid_for(n_cols_b, 256), 256, 0, st>>>((const long long*)prod_ptr, n_cols_b, n_tiles, tile_c0);
+  AS_LAUNCH_CHECK();
   ValSrc<double> vs{pvals, nullptr, (unsigned long long)total_products};
-  return launch_seg_engine<double>((const long long*)prod_ptr, n_cols_b, total_products, keys, keys_alt,
+  return launch_seg_engine<double>((const long long*)prod_ptr, tile_c0, n_cols_b, total_products, keys, keys_alt,
                                    bits_for(n_rows_a > 0 ? n_rows_a - 1 : 0),
                                    bits_for(total_products > 0 ? total_products - 1 : 0), 1, vs, kSumSeq, 1, col_ptr,
                                    row_idx, out_vals, (long long*)info, states, ticket, st);

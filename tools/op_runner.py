@@ -1,0 +1,63 @@
+"""Run one hot-path op a few times on its BASELINE config (for ncu captures).
+
+    python tools/op_runner.py build|flush|transpose|spmm|trace|add|spgemm [reps]
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1805_03380_b200 import _kernels, synth  # noqa: E402
+
+
+def main():
+    op = sys.argv[1]
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    dev = torch.device("cuda")
+
+    def T(a, dt):
+        return torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
+
+    if op in ("build", "transpose"):
+        n_rows, n_cols, rows, cols, vals = synth.cfg1_triplets()
+        r, c, v = T(rows, torch.int32), T(cols, torch.int32), T(vals, torch.float64)
+        p, ri, vv, _ = _kernels.coo_to_csc(n_rows, n_cols, r, c, v)
+        for _ in range(reps):
+            if op == "build":
+                _kernels.coo_to_csc(n_rows, n_cols, r, c, v)
+            else:
+                _kernels.transpose(n_rows, n_cols, p, ri, vv)
+    elif op == "flush":
+        n, _, rows, cols, vals = synth.cfg2_writes()
+        base = (torch.zeros(n + 1, dtype=torch.int32, device=dev), torch.empty(0, dtype=torch.int32, device=dev),
+                torch.empty(0, dtype=torch.float64, device=dev))
+        for _ in range(reps):
+            _kernels.flush_log(n, n, base, T(rows, torch.int32), T(cols, torch.int32), T(vals, torch.float64))
+    elif op == "spmm":
+        n, _, av, ar, ao, B = synth.cfg3_spmm()
+        csr = _kernels.transpose(n, n, T(ao, torch.int32), T(ar, torch.int32), T(av, torch.float32))
+        Bd = torch.as_tensor(B.T.copy(), device=dev).t()
+        for _ in range(reps):
+            _kernels.spmm(n, n, csr, Bd)
+    elif op in ("trace", "add", "spgemm"):
+        if op == "trace":
+            n, _, A, B = synth.cfg4_trace_pair()
+        else:
+            n, _, A, B = synth.cfg5_pair()
+        a = (T(A[2], torch.int32), T(A[1], torch.int32), T(A[0], torch.float64))
+        b = (T(B[2], torch.int32), T(B[1], torch.int32), T(B[0], torch.float64))
+        for _ in range(reps):
+            if op == "trace":
+                _kernels.fused_trace(n, n, a, b)
+            elif op == "add":
+                _kernels.linear_combine(n, n, a, b, 1.0, 1.0)
+            else:
+                _kernels.spgemm(n, n, n, a, b)
+    torch.cuda.synchronize()
+    print("ok", op)
+
+
+if __name__ == "__main__":
+    main()
