@@ -1,0 +1,116 @@
+"""Drop-in replacement for the reference's flat-array kernel module.
+
+`autosparse._kernels` (reference _kernels.py:1-175) is the de-facto operator
+boundary of the reference: plain numpy arrays in -- values
+float64, row indices / column offsets int64 -- fresh numpy arrays out, no
+validation.  This module exposes the same functions with the same positional
+signatures and return conventions, executed by the sm_100a kernels of
+libbsparse.so: inputs are copied to HBM, one C-ABI call runs, the result is
+copied back.  `canonicalize` and `rbt_to_csc` cover the other two entry points
+of the path (csc.canonicalize csc.py:148-193, rbt.to_csc rbt.py:444-458).
+
+It lets a reference user switch back ends with one assignment:
+
+    import autosparse, paper_1805_03380_b200.ref_kernels as k
+    autosparse.ops._kernels = k          # ops.add / matmul / transpose / SpMV
+    autosparse.expr._kernels = k         # fused trace
+
+(see INTEGRATION.md).  Every call needs a CUDA device; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _kernels
+
+_DEV = None
+
+
+def _dev():
+    global _DEV
+    if _DEV is None:
+        _DEV = torch.device("cuda", torch.cuda.current_device())
+    return _DEV
+
+
+def _i32(a):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32)).to(_dev())
+
+
+def _f64(a):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to(_dev())
+
+
+def _csc(vals, rows, offs):
+    return _i32(offs), _i32(rows), _f64(vals)
+
+
+def _out(p, r, v):
+    """(values f64, row_indices i64, col_offsets i64) numpy, the reference's
+    return order."""
+    return v.cpu().numpy().astype(np.float64), r.cpu().numpy().astype(np.int64), p.cpu().numpy().astype(np.int64)
+
+
+def linear_combine(n_cols, a_vals, a_rows, a_offs, b_vals, b_rows, b_offs, alpha, beta):
+    """_kernels.linear_combine (_kernels.py:12-48)."""
+    n_rows = int(max(np.max(a_rows, initial=-1), np.max(b_rows, initial=-1)) + 1)
+    p, r, v = _kernels.linear_combine(n_rows, n_cols, _csc(a_vals, a_rows, a_offs), _csc(b_vals, b_rows, b_offs),
+                                      alpha, beta)
+    return _out(p, r, v)
+
+
+def spgemm(n_rows_a, a_vals, a_rows, a_offs, b_vals, b_rows, b_offs, n_cols_b):
+    """_kernels.spgemm (_kernels.py:51-103)."""
+    n_inner = int(np.asarray(a_offs).shape[0] - 1)
+    p, r, v = _kernels.spgemm(n_rows_a, n_inner, n_cols_b, _csc(a_vals, a_rows, a_offs),
+                              _csc(b_vals, b_rows, b_offs))
+    return _out(p, r, v)
+
+
+def vec_times_mat(v, vals, rows, offs, n_cols):
+    """_kernels.vec_times_mat (_kernels.py:106-115)."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    w = _kernels.vec_times_mat(v.shape[0], n_cols, _csc(vals, rows, offs), _f64(v))
+    return w.cpu().numpy()
+
+
+def mat_times_vec(vals, rows, offs, x, n_rows, n_cols):
+    """_kernels.mat_times_vec (_kernels.py:118-127); the CSR it runs on is
+    built on the device for this call (the hybrid SpMat caches it)."""
+    csr = _kernels.transpose(n_rows, n_cols, *_csc(vals, rows, offs))
+    y = _kernels.mat_times_vec(n_rows, n_cols, csr, _f64(x))
+    return y.cpu().numpy()
+
+
+def transpose(n_rows, n_cols, vals, rows, offs):
+    """_kernels.transpose (_kernels.py:130-150)."""
+    return _out(*_kernels.transpose(n_rows, n_cols, *_csc(vals, rows, offs)))
+
+
+def fused_trace(n_cols, a_vals, a_rows, a_offs, b_vals, b_rows, b_offs):
+    """_kernels.fused_trace (_kernels.py:153-175)."""
+    n_rows = int(max(np.max(a_rows, initial=-1), np.max(b_rows, initial=-1)) + 1)
+    out = _kernels.fused_trace(n_rows, n_cols, _csc(a_vals, a_rows, a_offs), _csc(b_vals, b_rows, b_offs))
+    return float(out[0].item())
+
+
+def canonicalize(n_rows, n_cols, rows, cols, values, dup="sum"):
+    """csc.canonicalize (csc.py:148-193) on flat arrays; returns
+    (values, row_indices, col_offsets)."""
+    r = torch.as_tensor(np.ascontiguousarray(rows, dtype=np.int64)).to(_dev())
+    c = torch.as_tensor(np.ascontiguousarray(cols, dtype=np.int64)).to(_dev())
+    p, ri, v, bad = _kernels.coo_to_csc(n_rows, n_cols, r, c, _f64(values), dup)
+    if bad is not None:
+        raise IndexError("coordinate %d outside %dx%d matrix" % (bad, n_rows, n_cols))
+    return _out(p, ri, v)
+
+
+def rbt_to_csc(n_rows, n_cols, base, log_rows, log_cols, log_vals):
+    """rbt.to_csc (rbt.py:444-458) of the tree reached from the base CSC
+    (values, row_indices, col_offsets) by the element writes in the log."""
+    p, r, v, bad = _kernels.flush_log(n_rows, n_cols, _csc(*base), _i32(log_rows), _i32(log_cols), _f64(log_vals))
+    if bad is not None:
+        raise IndexError("write %d outside %dx%d matrix" % (bad, n_rows, n_cols))
+    return _out(p, r, v)
