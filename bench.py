@@ -179,8 +179,15 @@ def main_device(args):
     peak, peak_src = peaks()
     flush_buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
+    flush_scratch = torch.empty(1, dtype=torch.int64, device=dev)
+
     def l2_flush():
-        flush_buf.fill_(1)
+        # evict L2 by READING 512 MiB (a write-based flush leaves L2 full of
+        # dirty lines whose write-back would be charged to the timed kernel)
+        if args.flush == "write":
+            flush_buf.fill_(1)
+        else:
+            torch.sum(flush_buf.view(torch.int64), dim=0, out=flush_scratch)
 
     def timed(fn, steps, warmup):
         for _ in range(warmup):
@@ -309,7 +316,7 @@ def main_device(args):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded uniform triplets (SURVEY App. A); each rank its own batch (seed 1+rank)",
             "config": {"workload": HEADLINE, "n_rows": n_rows, "n_cols": n_cols, "triplets": n, "nnz_out": nnz,
-                       "index_dtype": "int32 device", "l2": "flushed before every step (512 MiB device write)",
+                       "index_dtype": "int32 device", "l2": "flushed before every step (512 MiB device read, %s)" % args.flush,
                        "parallelism": "independent batch per GPU" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": build_gbs, "peak": peak, "unit": "GB/s",
                          "frac": build_gbs / peak, "traffic": None, "peak_source": peak_src,
@@ -545,6 +552,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--skip-slow-checks", action="store_true")
+    ap.add_argument("--flush", default="read", choices=["read", "write"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

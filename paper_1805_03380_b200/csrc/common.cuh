@@ -246,4 +246,37 @@ AS_DEVICE_INLINE unsigned lanemask_lt() {
   return m;
 }
 
+// ------------------------------------------------------------------------
+// grid barrier for cooperatively launched (co-resident) grids
+struct GridBar {
+  unsigned* arrive;
+  unsigned* gen;
+};
+
+// Sense-free grid barrier for a cooperatively launched (co-resident) grid.
+AS_DEVICE_INLINE unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+AS_DEVICE_INLINE void grid_sync(const GridBar& gb, unsigned& gen_local) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned a = atomicAdd(gb.arrive, 1u);
+    if (a == gridDim.x - 1) {
+      *((volatile unsigned*)gb.arrive) = 0u;
+      __threadfence();
+      atomicAdd(gb.gen, 1u);
+    } else {
+      while (*((volatile unsigned*)gb.gen) == gen_local) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  gen_local++;
+  __syncthreads();
+}
+
+
 }  // namespace as

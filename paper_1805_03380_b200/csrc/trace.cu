@@ -13,11 +13,14 @@
 // left fold (_kernels.py:158-168) differs from it only by its own rounding.
 #include "capi_util.cuh"
 #include "common.cuh"
+#include "merge.cuh"
+
+#include <climits>
 
 namespace as {
 
 constexpr int kTrThreads = 256;
-constexpr int kTrItems = 16;
+constexpr int kTrItems = 32;
 constexpr int kTrChunk = kTrThreads * kTrItems;
 
 struct DD {
@@ -30,6 +33,13 @@ AS_DEVICE_INLINE void dd_add(DD& a, double p) {
   double err = __dadd_rn(__dsub_rn(a.s, __dsub_rn(t, bp)), __dsub_rn(p, bp));
   a.s = t;
   a.e = __dadd_rn(a.e, err);
+}
+
+// the (rare) match path kept out of line so the pointer-advance loop is not
+// if-converted into predicated double-double arithmetic on every step
+__device__ __noinline__ void dd_add_match(DD& acc, const double* __restrict__ av, const double* __restrict__ bv,
+                                          int ia, int ib) {
+  dd_add(acc, __dmul_rn(__ldg(&av[ia]), __ldg(&bv[ib])));
 }
 
 AS_DEVICE_INLINE DD dd_merge(DD a, DD b) {
@@ -45,98 +55,70 @@ AS_DEVICE_INLINE DD dd_shfl_xor(DD a, int o) {
   return r;
 }
 
-// merged start of column c
-AS_DEVICE_INLINE long long mstart(const int* ap, const int* bp, long long c) {
-  return (long long)ap[c] + (long long)bp[c];
-}
+// One warp per column pair (grid-stride over columns): the longer of the
+// two row lists is staged in the warp's shared-memory buffer (coalesced),
+// every lane takes elements of the shorter list (coalesced) and does a
+// branch-free lower_bound there; values are read only at matches.  Columns
+// whose longer list exceeds the buffer are searched in global memory.
+// (Measured alternatives on cfg 4: per-thread merge path over the
+// concatenated columns 90-96 us, lane-per-column sequential merge 127 us.)
+constexpr int kTrWarpBuf = 1024;
 
 __global__ void __launch_bounds__(kTrThreads)
 trace_partial_kernel(long long n_cols, const int* __restrict__ ap, const int* __restrict__ ar,
                      const double* __restrict__ av, const int* __restrict__ bp, const int* __restrict__ br,
                      const double* __restrict__ bv, DD* partials, unsigned* done, double* out) {
-  __shared__ long long s_clo, s_chi;
+  __shared__ int sbuf[kTrThreads / 32][kTrWarpBuf];
   __shared__ DD s_warp[kTrThreads / 32];
   __shared__ bool s_last;
-  const long long M = mstart(ap, bp, n_cols);
-  const long long cbase = (long long)blockIdx.x * kTrChunk;
-  const long long cend = min(cbase + kTrChunk, M);
-  if (threadIdx.x == 0) {
-    // last column whose merged start <= cbase, and the one holding cend-1
-    long long lo = 0, hi = n_cols;
-    while (lo < hi) {
-      long long mid = (lo + hi + 1) >> 1;
-      if (mstart(ap, bp, mid) <= cbase) lo = mid;
-      else hi = mid - 1;
-    }
-    s_clo = lo;
-    long long lo2 = lo, hi2 = n_cols;
-    while (lo2 < hi2) {
-      long long mid = (lo2 + hi2 + 1) >> 1;
-      if (mstart(ap, bp, mid) <= cend - 1) lo2 = mid;
-      else hi2 = mid - 1;
-    }
-    s_chi = lo2;
-  }
-  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long nwarps = (long long)gridDim.x * (kTrThreads / 32);
   DD acc{0.0, 0.0};
-  const long long d0 = cbase + (long long)threadIdx.x * kTrItems;
-  const long long d1 = min(d0 + kTrItems, cend);
-  if (d0 < d1) {
-    // column holding d0: last c in [clo, chi] with mstart(c) <= d0
-    long long lo = s_clo, hi = s_chi;
-    while (lo < hi) {
-      long long mid = (lo + hi + 1) >> 1;
-      if (mstart(ap, bp, mid) <= d0) lo = mid;
-      else hi = mid - 1;
-    }
-    long long c = lo;
-    long long a0 = ap[c], b0 = bp[c];
-    long long la = ap[c + 1] - a0, lb = bp[c + 1] - b0;
-    long long dl = d0 - (a0 + b0);
-    // merge-path split with A winning ties
-    long long i_lo = max(0ll, dl - lb), i_hi = min(dl, la);
-    while (i_lo < i_hi) {
-      long long mid = (i_lo + i_hi) >> 1;
-      if (ar[a0 + mid] <= br[b0 + dl - mid - 1]) i_lo = mid + 1;
-      else i_hi = mid;
-    }
-    long long i = i_lo, j = dl - i_lo;
-    // an equal pair split at our start was consumed by the previous thread
-    if (i > 0 && j < lb && br[b0 + j] == ar[a0 + i - 1]) j++;
-    long long pos = a0 + b0 + i + j;
-    while (pos < d1) {
-      if (i == la && j == lb) {
-        c++;
-        a0 = ap[c];
-        b0 = bp[c];
-        la = ap[c + 1] - a0;
-        lb = bp[c + 1] - b0;
-        i = j = 0;
-        continue;
-      }
-      if (j == lb) {
-        i++;
-      } else if (i == la) {
-        j++;
-      } else {
-        int ra = ar[a0 + i], rb = br[b0 + j];
-        if (ra == rb) {
-          dd_add(acc, __dmul_rn(av[a0 + i], bv[b0 + j]));
-          i++;
-          j++;
-        } else if (ra < rb) {
-          i++;
-        } else {
-          j++;
+  int* buf = sbuf[wib];
+  for (long long c = (long long)blockIdx.x * (kTrThreads / 32) + wib; c < n_cols; c += nwarps) {
+    const int a0 = __ldg(&ap[c]), a1 = __ldg(&ap[c + 1]), b0 = __ldg(&bp[c]), b1 = __ldg(&bp[c + 1]);
+    const int la = a1 - a0, lb = b1 - b0;
+    if (la == 0 || lb == 0) continue;
+    const bool a_long = la >= lb;
+    const int* Lr = a_long ? ar : br;
+    const int* Sr = a_long ? br : ar;
+    const double* Lv = a_long ? av : bv;
+    const double* Sv = a_long ? bv : av;
+    const int l0 = a_long ? a0 : b0, ll = a_long ? la : lb;
+    const int s0 = a_long ? b0 : a0, sl = a_long ? lb : la;
+    if (ll <= kTrWarpBuf) {
+      for (int q = lane; q < ll; q += 32) buf[q] = __ldg(&Lr[l0 + q]);
+      __syncwarp();
+      int span = 1;
+      while (span < ll) span <<= 1;
+      for (int q = lane; q < sl; q += 32) {
+        const int r = __ldg(&Sr[s0 + q]);
+        int pos = 0;
+        for (int step = span >> 1; step > 0; step >>= 1) {
+          const int probe = pos + step;
+          pos = (probe <= ll && buf[probe - 1] < r) ? probe : pos;
         }
+        if (pos < ll && buf[pos] == r) dd_add_match(acc, Lv, Sv, l0 + pos, s0 + q);
       }
-      pos = a0 + b0 + i + j;
+    } else {
+      const int* L = Lr + l0;
+      for (int q = lane; q < sl; q += 32) {
+        const int r = __ldg(&Sr[s0 + q]);
+        int lo = 0, hi = ll;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (__ldg(&L[mid]) < r) lo = mid + 1;
+          else hi = mid;
+        }
+        if (lo < ll && __ldg(&L[lo]) == r) dd_add_match(acc, Lv, Sv, l0 + lo, s0 + q);
+      }
     }
+    __syncwarp();
   }
   // deterministic block reduction
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc = dd_merge(acc, dd_shfl_xor(acc, o));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = wib;
   if (lane == 0) s_warp[warp] = acc;
   __syncthreads();
   if (warp == 0) {
@@ -161,12 +143,25 @@ trace_partial_kernel(long long n_cols, const int* __restrict__ ap, const int* __
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = dd_merge(v, dd_shfl_xor(v, o));
     if (lane == 0) {
-      double hi = __dadd_rn(v.s, v.e);
-      double lo = __dsub_rn(v.e, __dsub_rn(hi, v.s));
-      out[0] = hi;
-      out[1] = lo;
+      double hi2 = __dadd_rn(v.s, v.e);
+      double lo2 = __dsub_rn(v.e, __dsub_rn(hi2, v.s));
+      out[0] = hi2;
+      out[1] = lo2;
     }
   }
+}
+
+static int trace_grid() {
+  static int grid = 0;
+  if (grid == 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_partial_kernel, kTrThreads, 0);
+    per_sm = std::min(per_sm, 6);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = std::max(1, per_sm * sms);
+  }
+  return grid;
 }
 
 }  // namespace as
@@ -176,9 +171,10 @@ using namespace as;
 extern "C" {
 
 size_t as_trace_workspace_bytes(int64_t n_cols, int64_t nnz_a, int64_t nnz_b) {
-  long long M = nnz_a + nnz_b;
-  long long blocks = M > 0 ? (M + kTrChunk - 1) / kTrChunk : 1;
-  return 256 + ((size_t)blocks * sizeof(DD) + 255) / 256 * 256;
+  (void)n_cols;
+  (void)nnz_a;
+  (void)nnz_b;
+  return 256 + (size_t)148 * 32 * sizeof(DD);  // partials of the largest co-resident grid
 }
 
 int as_trace_atb_f64(int64_t n_rows, int64_t n_cols, const int32_t* a_col_ptr, const int32_t* a_row_idx,
@@ -187,8 +183,7 @@ int as_trace_atb_f64(int64_t n_rows, int64_t n_cols, const int32_t* a_col_ptr, c
   cudaStream_t st = S(stream);
   AS_REQUIRE(n_cols >= 0 && n_rows >= 0, AS_ERR_SHAPE, "negative dimension");
   AS_REQUIRE(ws_bytes >= as_trace_workspace_bytes(n_cols, nnz_a, nnz_b), AS_ERR_ARG, "workspace too small");
-  long long M = nnz_a + nnz_b;
-  long long blocks = M > 0 ? (M + kTrChunk - 1) / kTrChunk : 1;
+  const long long blocks = std::min(trace_grid(), 148 * 32);
   unsigned* done = (unsigned*)ws;
   DD* partials = (DD*)((char*)ws + 256);
   AS_CUDA_TRY(cudaMemsetAsync(done, 0, sizeof(unsigned), st));
