@@ -19,57 +19,56 @@ namespace as {
 
 constexpr long long kMaxDim = 0x7fffffffll;
 constexpr long long kMaxGrid = 148 * 8;  // upper bound of the co-resident grid
-constexpr long long kNprMax = 64;        // chunk ranges of the phase-2 work items
 
 struct PersistWs {
-  unsigned* zero;  // [0] ticket, [16] barrier arrive, [32] barrier generation
-  unsigned* counts;
+  unsigned* zero;  // [0] ticket, [16] barrier arrive, [32] barrier generation, then cb_cnt
+  unsigned* cb_cnt;
   size_t zero_bytes;
-  unsigned* partials;
-  unsigned* range_sum;
-  long long* cta_sums;
-  long long* seg_ptr;
-  long long* tile_c0;
-  long long* tile_total;
+  long long* cb_start;
   unsigned long long* keys;
   unsigned long long* keys_alt;
+  unsigned* colb;
+  unsigned* colb_alt;
   void* vals_b;
   int* tmp_rows;
   void* tmp_vals;
-  long long n_tiles, P1;
-  int smem_hist;
+  unsigned* col_kept;
+  long long* cta_sums;
+  long long* own_info;
+  int wbits;
+  long long n_cb;
 };
 
-// histogram chunks: one per CTA of the co-resident grid (<= 3 x 148) so the
-// histogram and scatter phases use every SM; >= 256 elements per chunk and
-// the partials matrix capped at 8M entries.
-static inline long long choose_p1(long long n, long long nb) {
-  if (nb <= 0) return 1;
-  long long p = std::min(444ll, std::max(1ll, n / 256));
-  p = std::min(p, std::max(1ll, (8ll << 20) / nb));
-  return p;
+// Coarse buckets of W = 2^wbits output columns: ~0.8 * kCap elements per
+// bucket on average, at most kMaxCoarse buckets.  Returns -1 when the column
+// count exceeds kMaxCoarse * kMaxW.
+static inline int choose_wbits(long long n, long long n_cols) {
+  const double avg = n_cols > 0 ? (double)n / (double)n_cols : 0.0;
+  int wb = 0;
+  while ((1 << (wb + 1)) <= kMaxW && (double)(1 << (wb + 1)) * avg <= 0.8 * kCap) wb++;
+  while (wb <= 10 && ((n_cols + (1ll << wb) - 1) >> wb) > kMaxCoarse) wb++;
+  return ((n_cols + (1ll << wb) - 1) >> wb) > kMaxCoarse || (1 << wb) > kMaxW ? -1 : wb;
 }
 
-static size_t carve_persist(Carve& c, PersistWs* w, long long n, long long nb, size_t val_bytes) {
-  w->n_tiles = seg_engine_tiles(n);
-  w->smem_hist = (nb <= kHistMaxBins && n >= nb) ? 1 : 0;
-  w->P1 = w->smem_hist ? choose_p1(n, nb) : 1;
+static size_t carve_persist(Carve& c, PersistWs* w, long long n, long long n_cols, size_t val_bytes) {
+  w->wbits = choose_wbits(n, n_cols);
+  const int wb = w->wbits < 0 ? 10 : w->wbits;
+  w->n_cb = (n_cols + (1ll << wb) - 1) >> wb;
   w->zero = c.take<unsigned>(64);
-  w->counts = c.take<unsigned>(w->smem_hist ? 1 : std::max(1ll, nb));
+  w->cb_cnt = c.take<unsigned>(std::max(1ll, w->n_cb));
   w->zero_bytes = c.off;
-  w->partials = c.take<unsigned>(w->smem_hist ? w->P1 * nb : 1);
-  w->range_sum = c.take<unsigned>(w->smem_hist ? kNprMax * nb : 1);
-  w->cta_sums = c.take<long long>(2 * kMaxGrid);
-  w->seg_ptr = c.take<long long>(nb + 1);
-  w->tile_c0 = c.take<long long>(w->n_tiles + 1);
-  w->tile_total = c.take<long long>(w->n_tiles);
+  w->cb_start = c.take<long long>(w->n_cb + 1);
   const long long n1 = std::max(1ll, n);
   w->keys = c.take<unsigned long long>(n1);
   w->keys_alt = c.take<unsigned long long>(n1);
+  w->colb = c.take<unsigned>(n1);
+  w->colb_alt = c.take<unsigned>(n1);
   w->vals_b = (void*)c.take<char>(n1 * val_bytes);
   w->tmp_rows = c.take<int>(n1);
   w->tmp_vals = (void*)c.take<char>(n1 * val_bytes);
-  c.take<long long>(2);
+  w->col_kept = c.take<unsigned>(std::max(1ll, n_cols));
+  w->cta_sums = c.take<long long>(kMaxGrid);
+  w->own_info = c.take<long long>(2);
   return c.off;
 }
 
@@ -93,39 +92,37 @@ static int launch_persist(PersistArgs<T, S1, S2>& a, cudaStream_t st) {
 }
 
 template <class T, class S1, class S2>
-static int run_persist(const S1& s1, const S2& s2, long long nb, int row_bits, int mode, int prune, ValSrc<T> vs,
+static int run_persist(const S1& s1, const S2& s2, long long n_cols, int row_bits, int mode, int prune, ValSrc<T> vs,
                        int* col_ptr, int* row_idx, T* out_vals, long long* info, bool init_info, void* ws,
                        size_t ws_bytes, cudaStream_t st) {
   const long long n = s1.size() + s2.size();
   Carve c(ws, ws_bytes);
   PersistWs w;
-  carve_persist(c, &w, n, nb, sizeof(T));
-  long long* own_info = (long long*)(c.base ? c.base + c.off - 256 : nullptr);
+  carve_persist(c, &w, n, n_cols, sizeof(T));
   AS_REQUIRE(c.ok, AS_ERR_ARG, "workspace too small: %zu < %zu", ws_bytes, c.off);
-  if (info == nullptr) info = own_info;
+  AS_REQUIRE(w.wbits >= 0, AS_ERR_ARG, "%lld output columns exceed the %lld supported by the bucket kernel",
+             n_cols, (long long)kMaxCoarse * kMaxW);
+  if (info == nullptr) info = w.own_info;
   AS_CUDA_TRY(cudaMemsetAsync(w.zero, 0, w.zero_bytes, st));
   if (init_info) AS_CUDA_TRY(cudaMemsetAsync(info, 0x7f, 2 * sizeof(long long), st));
   PersistArgs<T, S1, S2> a;
   a.s1 = s1;
   a.s2 = s2;
-  a.n_bins = nb;
+  a.n_cols = n_cols;
   a.n_upper = n;
-  a.P1 = w.P1;
-  a.smem_hist = w.smem_hist;
-  a.partials = w.partials;
-  a.counts = w.counts;
-  a.range_sum = w.range_sum;
-  a.n_pr_max = kNprMax;
-  a.cta_sums = w.cta_sums;
-  a.seg_ptr = w.seg_ptr;
-  a.tile_c0 = w.tile_c0;
-  a.n_tiles = w.n_tiles;
-  a.tile_total = w.tile_total;
+  a.wbits = w.wbits;
+  a.n_cb = w.n_cb;
+  a.cb_cnt = w.cb_cnt;
+  a.cb_start = w.cb_start;
   a.keys = w.keys;
   a.keys_alt = w.keys_alt;
+  a.colb = w.colb;
+  a.colb_alt = w.colb_alt;
   a.vals_b = (T*)w.vals_b;
   a.tmp_rows = w.tmp_rows;
   a.tmp_vals = (T*)w.tmp_vals;
+  a.col_kept = w.col_kept;
+  a.cta_sums = w.cta_sums;
   a.row_bits = row_bits;
   a.idx_bits = bits_for(n > 0 ? n - 1 : 0);
   a.mode = mode;
@@ -150,17 +147,17 @@ static int run_persist(const S1& s1, const S2& s2, long long nb, int row_bits, i
     unsigned long long h[16];
     AS_CUDA_TRY(cudaMemcpyAsync(h, dbg_ts, sizeof(h), cudaMemcpyDeviceToHost, st));
     AS_CUDA_TRY(cudaStreamSynchronize(st));
-    fprintf(stderr, "[phases n=%lld nb=%lld smem_hist=%d P1=%lld]", n, nb, w.smem_hist, w.P1);
+    fprintf(stderr, "[phases n=%lld n_cols=%lld W=%d n_cb=%lld]", n, n_cols, 1 << w.wbits, w.n_cb);
     for (int i = 1; i < 16 && h[i]; i++) fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
     fprintf(stderr, " us\n");
   }
   return rc;
 }
 
-size_t persist_ws_bytes(long long n, long long nb, size_t val_bytes) {
+size_t persist_ws_bytes(long long n, long long n_cols, size_t val_bytes) {
   Carve c(nullptr, 0);
   PersistWs w;
-  carve_persist(c, &w, n, nb, val_bytes);
+  carve_persist(c, &w, n, n_cols, val_bytes);
   return c.off;
 }
 

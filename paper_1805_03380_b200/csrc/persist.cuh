@@ -3,40 +3,43 @@
 // CSC transpose).
 //
 // At the sizes of the BASELINE configs (1e5-1e7 elements) a pipeline of
-// separate kernels is latency bound: every kernel boundary drains the GPU,
-// and per-element global atomics on ~1e4 buckets serialise in L2 (measured
-// on B200: 1M RED.ADD over 10k bins take ~24 us, tools/micro/atomic_micro.cu).
-// Here the whole operation is one launch of exactly the co-resident grid
-// (148 SMs x blocks/SM), phases separated by a grid barrier:
+// separate kernels is latency bound, and per-element global atomics on ~1e4
+// buckets serialise in L2 (measured on B200: 1M RED.ADD over 10k bins take
+// ~24 us, tools/micro/atomic_micro.cu).  Here the whole operation is one
+// launch of exactly the co-resident grid, phases separated by grid barriers:
 //
-//   1 histogram   P1 chunks of the input, each counted in a shared-memory
-//                 histogram, written as one row of partials[P1][n_bins]
-//                 (no per-element global atomics); falls back to global
-//                 atomics when n_bins exceeds the shared-memory histogram
-//   2 scan        grid-wide exclusive scan of the bucket totals -> seg_ptr;
-//                 partials rewritten in place as per-(chunk, bucket) bases;
-//                 the tile -> segment map for phase 4
-//   3 scatter     each chunk re-read; slot = shared-memory cursor; the key
-//                 (minor << 32 | input index) and the VALUE move to the slot,
-//                 so the tile phase reads values contiguously from L2
-//   4 tiles       the segmented sort / run-reduce engine (segsort.cuh) on
-//                 claimed tiles, compacted output into temporaries at the
-//                 tile's own offset, tile totals recorded (no look-back chain)
-//   5 place       grid-wide scan of tile totals; each tile copied to its final
-//                 offset and its col_ptr entries shifted by the tile prefix
+//   1 coarse histogram  buckets = W consecutive output columns (W chosen so a
+//                       bucket holds ~1k elements and there are <= 8192 of
+//                       them); each CTA counts its chunk in shared memory and
+//                       reserves its range inside every non-empty bucket with
+//                       ONE global atomic per bucket.           [grid barrier]
+//   2 coarse scan       every CTA scans the bucket counts itself (no barrier)
+//   3 scatter           each chunk re-read; slot = bucket start + CTA range +
+//                       shared cursor; key (row << 32 | input index), column
+//                       and value moved to the slot.            [grid barrier]
+//   4 bucket tiles      a CTA per bucket sorts it by (column, row, input
+//                       order) in shared memory -- bins (column, high row
+//                       bits) of ~4 keys, every key ranking itself in its bin
+//                       -- reduces runs in the reference order, prunes zeros,
+//                       writes the compacted bucket to temporaries and the
+//                       kept count of each column.  Buckets larger than the
+//                       tile are radix-sorted in global memory and streamed.
+//                                                               [grid barrier]
+//   5 columns           grid-wide scan of the kept counts -> col_ptr; each
+//                       bucket copied to its final offset.      [2 barriers]
 #pragma once
 
 #include "segsort.cuh"
 
 namespace as {
 
-#define AS_PHASE_MARK(a, gen)                                                       \
-  do {                                                                              \
-    if ((a).phase_ts && blockIdx.x == 0 && threadIdx.x == 0) (a).phase_ts[gen] = global_ns(); \
+#define AS_PHASE_MARK(a, gen)                                                                   \
+  do {                                                                                          \
+    if ((a).phase_ts && blockIdx.x == 0 && threadIdx.x == 0) (a).phase_ts[gen] = global_ns();   \
   } while (0)
 
 // ------------------------------------------------------------------------
-// element sources: visit(p, P, f) calls f(bucket, minor, idx, i) for every
+// element sources: visit(p, P, report, f) calls f(col, row, idx, i) for every
 // valid element of chunk p of P (the same partition every time it is called)
 
 constexpr int kVisitVec = 4;  // consecutive elements per thread (ILP)
@@ -72,8 +75,6 @@ struct CooSrc {
   unsigned long long idx_off;
   long long* bad;  // first invalid triplet (reported in phase 1)
 
-  // chunk p of P: elements [p*ch, min(n, (p+1)*ch)), ch a multiple of 4;
-  // each thread takes 4 consecutive elements per step (vector loads).
   template <class F>
   __device__ void visit(long long p, long long P, bool report, F f) const {
     const long long ch = (((n + P - 1) / P) + 3) & ~3ll;
@@ -99,11 +100,10 @@ struct CooSrc {
   AS_DEVICE_INLINE void set_cache(int*) {}
 };
 
-// The elements of a CSC: by_row = false -> bucket col, minor row (flush
-// base); by_row = true -> bucket row, minor col (transpose).  Chunk p is the
-// element range [p*ch, (p+1)*ch); the columns it touches are staged in
-// shared memory (colc) when they fit, and each thread finds the column of
-// its 4 consecutive elements by binary search there (or in global memory).
+// The elements of a CSC: by_row = false -> output column = col, minor = row
+// (flush base); by_row = true -> output column = row, minor = col (transpose).
+// Chunk p is the element range [p*ch, (p+1)*ch); the column starts it spans
+// are staged in shared memory (colc) when they fit.
 constexpr int kColCache = 1024;
 
 template <class T>
@@ -115,7 +115,7 @@ struct CscSrc {
   long long nnz;
   bool by_row;
   unsigned long long idx_off;
-  int* colc;  // shared-memory column-start cache (kColCache + 1 entries), set by the kernel
+  int* colc;
 
   template <class F>
   __device__ void visit(long long p, long long P, bool report, F f) const {
@@ -126,8 +126,8 @@ struct CscSrc {
     const long long lo = min(nnz, p * ch), hi = min(nnz, lo + ch);
     __syncthreads();
     if (threadIdx.x == 0 && lo < hi) {
-      s_cb = upper_bound_dev(col_ptr, n_cols + 1, (int)lo) - 1;      // column holding lo
-      s_ce = upper_bound_dev(col_ptr, n_cols + 1, (int)(hi - 1));    // one past the column holding hi-1
+      s_cb = upper_bound_dev(col_ptr, n_cols + 1, (int)lo) - 1;
+      s_ce = upper_bound_dev(col_ptr, n_cols + 1, (int)(hi - 1));
     }
     __syncthreads();
     if (lo >= hi) return;
@@ -139,7 +139,7 @@ struct CscSrc {
     for (long long i = lo + (long long)threadIdx.x * kVisitVec; i < hi; i += (long long)blockDim.x * kVisitVec) {
       long long c;
       if (cached) {
-        int l = 0, h = (int)(ce - cb);  // last q with colc[q] <= i
+        int l = 0, h = (int)(ce - cb);
         while (l < h) {
           const int mid = (l + h + 1) >> 1;
           if (colc[mid] <= i) l = mid;
@@ -176,33 +176,33 @@ struct NoSrc {
   AS_DEVICE_INLINE void set_cache(int*) {}
 };
 
-constexpr int kHistMaxBins = 11264;  // shared-memory histogram capacity (44 KB)
+// ------------------------------------------------------------------------
+constexpr int kMaxCoarse = 8192;  // coarse buckets (two u32 arrays in smem)
+constexpr int kMaxW = 1024;       // columns per coarse bucket
+constexpr int kTBins = 1024;      // second-level bins per bucket tile
 
 template <class T, class S1, class S2>
 struct PersistArgs {
   S1 s1;
   S2 s2;
-  long long n_bins;
+  long long n_cols;   // output columns (fine buckets)
   long long n_upper;  // s1.size() + s2.size()
-  long long P1;       // histogram chunks (smem path)
-  int smem_hist;
-  unsigned* partials;  // [P1][n_bins]
-  unsigned* counts;    // [n_bins] (atomic path, zeroed)
-  unsigned* range_sum; // [n_pr_max][n_bins] (smem path)
-  long long n_pr_max;
-  long long* cta_sums; // [2 * grid]
-  long long* seg_ptr;  // [n_bins + 1]
-  long long* tile_c0;  // [n_tiles + 1]
-  long long n_tiles;
-  long long* tile_total;  // [n_tiles]
+  int wbits;          // coarse bucket = column >> wbits
+  long long n_cb;
+  unsigned* cb_cnt;       // [n_cb] zeroed
+  long long* cb_start;    // [n_cb + 1]
   unsigned long long* keys;
   unsigned long long* keys_alt;
-  T* vals_b;            // bucketed values (by slot)
+  unsigned* colb;         // output column of each bucketed element
+  unsigned* colb_alt;
+  T* vals_b;              // bucketed values (by slot)
   int* tmp_rows;
   T* tmp_vals;
+  unsigned* col_kept;     // [n_cols]
+  long long* cta_sums;    // [grid]
   int row_bits, idx_bits;
   int mode, prune;
-  ValSrc<T> vs;         // values by input index (oversized tiles)
+  ValSrc<T> vs;           // values by input index (oversized buckets)
   int* col_ptr;
   int* row_idx;
   T* out_vals;
@@ -213,221 +213,491 @@ struct PersistArgs {
 };
 
 template <class T>
-union PersistSmem {
-  struct {
-    unsigned hist[kHistMaxBins];
-    int colc[kColCache + 1];
-  } h;
-  SegSmem<T> seg;
+struct BTileSmem {
+  unsigned long long sk[kCap];
+  union {
+    T rv[kCap];
+    unsigned long long sk2[kCap];
+    struct {
+      unsigned hist[256];
+      unsigned wcnt[256 * (kSegThreads / 32)];
+    } rs;
+  } u;
+  union {
+    unsigned short excl[kCap + 8];
+    struct {
+      unsigned cursor[kTBins];
+      unsigned short bstart[kTBins + 8];
+    } bk;
+  } v;
+  unsigned short scol[kCap];   // local column of each key (sk order)
+  unsigned short perm[kCap];
+  unsigned short perm2[kCap];
+  unsigned short sbin[kCap];
+  unsigned short cstart[kMaxW + 8];  // column boundaries (tile positions)
+  unsigned hbits[kCap / 32];
+  short med[kTBins], big[kTBins];
+  int n_med, n_big;
+  long long scan_tmp[kSegThreads / 32 + 1];
+  unsigned ckept[kMaxW];  // kept per column (oversized path)
+  long long tile, s, m;
 };
 
-// grid-wide exclusive scan helper: CTA g owns items [g*per, min(n, (g+1)*per))
+template <class T>
+union PersistSmem {
+  struct {
+    unsigned a[kMaxCoarse];  // histogram, then shared cursor
+    unsigned b[kMaxCoarse];  // CTA range inside each bucket, then slot base
+    int colc[kColCache + 1];
+  } h;
+  BTileSmem<T> t;
+};
+
 AS_DEVICE_INLINE void cta_range(long long n, long long g, long long G, long long* lo, long long* hi) {
   const long long per = (n + G - 1) / G;
   *lo = min(n, g * per);
   *hi = min(n, *lo + per);
 }
 
+// Block-level stable LSD radix sort of (u64 key, u32 payload) pairs in global
+// memory; pass i sorts by bits [shift, shift+nbits) of the key (from_payload
+// = 0) or of the payload (1).  Leaves the result in (k, p).
+__device__ void block_radix_sort_kv(unsigned long long* k, unsigned* p, unsigned long long* k_alt, unsigned* p_alt,
+                                    long long L, const int* shifts, const int* nbits, const int* from_payload,
+                                    int npass, unsigned* hist, unsigned* wcnt) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+  unsigned long long *sk = k, *dk = k_alt;
+  unsigned *sp = p, *dp = p_alt;
+  for (int ps = 0; ps < npass; ps++) {
+    const int sh = shifts[ps];
+    const unsigned mask = (1u << nbits[ps]) - 1u;
+    const bool fp = from_payload[ps];
+    auto digit = [&](long long i) -> unsigned {
+      return fp ? ((sp[i] >> sh) & mask) : ((unsigned)(sk[i] >> sh) & mask);
+    };
+    for (int i = tid; i < 256; i += nthr) hist[i] = 0;
+    for (int i = tid; i < 256 * nwarps; i += nthr) wcnt[i] = 0;
+    __syncthreads();
+    for (long long i = tid; i < L; i += nthr) atomicAdd(&hist[digit(i)], 1u);
+    __syncthreads();
+    if (warp == 0) {
+      unsigned carry = 0;
+      for (int b = 0; b < 256; b += 32) {
+        const unsigned v = hist[b + lane];
+        const unsigned inc = warp_inclusive_scan(v);
+        hist[b + lane] = carry + inc - v;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+    }
+    __syncthreads();
+    for (long long base = 0; base < L; base += nthr) {
+      const long long i = base + tid;
+      const bool in = i < L;
+      const unsigned dg = in ? digit(i) : 0xffffffffu;
+      const unsigned act = __ballot_sync(0xffffffffu, in);
+      unsigned rank = 0;
+      if (in) {
+        const unsigned peers = __match_any_sync(act, dg);
+        rank = __popc(peers & lanemask_lt());
+        if (rank == 0) wcnt[warp * 256 + dg] = __popc(peers);
+      }
+      __syncthreads();
+      for (int b = tid; b < 256; b += nthr) {
+        unsigned run = hist[b];
+        for (int w = 0; w < nwarps; w++) {
+          const unsigned c = wcnt[w * 256 + b];
+          wcnt[w * 256 + b] = run;
+          run += c;
+        }
+        hist[b] = run;
+      }
+      __syncthreads();
+      if (in) {
+        const unsigned o = wcnt[warp * 256 + dg] + rank;
+        dk[o] = sk[i];
+        dp[o] = sp[i];
+      }
+      __syncthreads();
+      for (int b = tid; b < 256 * nwarps; b += nthr) wcnt[b] = 0;
+      __syncthreads();
+    }
+    unsigned long long* t1 = sk;
+    sk = dk;
+    dk = t1;
+    unsigned* t2 = sp;
+    sp = dp;
+    dp = t2;
+  }
+  if (sk != k) {
+    for (long long i = tid; i < L; i += nthr) {
+      k[i] = sk[i];
+      p[i] = sp[i];
+    }
+    __syncthreads();
+  }
+}
+
+// Reduce the runs of one chunk [b, b+cm) of a sorted bucket whose keys / local
+// columns are in S.sk / S.scol.  Runs end at a column or row change; a run
+// crossing the chunk end continues in global memory (gk, gcol; nullptr when
+// the chunk is the whole bucket).  vslot: values by tile slot through S.perm
+// (nullptr: values by input index).  Leaves S.u.rv[p] = run value at kept
+// heads, S.v.excl[0..cm] exclusive kept counts; returns the chunk total.
+template <class T, class VS>
+__device__ long long bucket_chunk_reduce(BTileSmem<T>& S, long long b, int cm, long long m,
+                                         const unsigned long long* gk, const unsigned* gcol, unsigned col_base,
+                                         VS vs, int mode, int prune, const T* vslot) {
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  for (int base = 0; base < cm; base += nthr) {
+    const int p = base + tid;
+    bool head = false;
+    if (p < cm) {
+      const unsigned long long k = S.sk[p];
+      const unsigned row = key_row(k), col = S.scol[p];
+      if (p > 0) head = row != key_row(S.sk[p - 1]) || col != S.scol[p - 1];
+      else head = (b == 0) || row != key_row(gk[b - 1]) || col != gcol[b - 1] - col_base;
+      S.u.rv[p] = vslot ? vslot[S.perm[p]] : vs((unsigned long long)key_idx(k));
+    }
+    const unsigned hb = __ballot_sync(0xffffffffu, head);
+    if (lane == 0 && base + warp * 32 < cm) S.hbits[(base >> 5) + warp] = hb;
+  }
+  __syncthreads();
+  const int pb = tid * kItems, pe = min(pb + kItems, cm);
+  int cnt = 0;
+  for (int p = pb; p < pe; p++) {
+    unsigned short f = 0;
+    if (bit_at(S.hbits, p)) {
+      const int q = next_bit(S.hbits, p + 1, cm);
+      T v;
+      if (q < cm || gk == nullptr || b + cm >= m) {
+        if (q == p + 1) {
+          v = S.u.rv[p];
+        } else {
+          const T* rvp = S.u.rv + p;
+          v = reduce_run<T>([&](long long i) -> T { return rvp[i]; }, q - p, mode);
+        }
+      } else {
+        const unsigned row = key_row(S.sk[p]), col = S.scol[p] + col_base;
+        long long qg = b + cm;
+        while (qg < m && key_row(gk[qg]) == row && gcol[qg] == col) qg++;
+        const T* rvp = S.u.rv + p;
+        const long long in_chunk = cm - p;
+        const unsigned long long* gkp = gk + b + p;
+        v = reduce_run<T>(
+            [&](long long i) -> T { return i < in_chunk ? rvp[i] : vs((unsigned long long)key_idx(gkp[i])); },
+            qg - (b + p), mode);
+      }
+      if (!prune || v != T(0)) {
+        f = 1;
+        S.u.rv[p] = v;
+      }
+    }
+    S.v.excl[p] = f;
+    cnt += f;
+  }
+  long long total;
+  const long long off = block_exclusive_scan<long long>((long long)cnt, S.scan_tmp, &total);
+  unsigned run = (unsigned)off;
+  for (int p = pb; p < pe; p++) {
+    const unsigned f = S.v.excl[p];
+    S.v.excl[p] = (unsigned short)run;
+    run += f;
+  }
+  if (tid == 0) S.v.excl[cm] = (unsigned short)total;
+  __syncthreads();
+  return total;
+}
+
+// Sort a bucket held in S.sk / S.scol (tile positions, perm = identity) by
+// (column, row, input order): bins (column, high row bits) of ~4 keys,
+// counting pass, scan, scatter to S.u.sk2, then rank-in-bin placement back
+// into S.sk (long bins: warp / block bitonic).  Leaves S.scol in sorted order
+// and S.cstart[l] = first position of local column l (l = 0..W).
+template <class T>
+__device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int W, int row_bits) {
+  const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
+  int lr = 0;
+  while (lr < row_bits && W * (2 << lr) <= kTBins && W * (2 << lr) * 4 <= m) lr++;
+  const int R = 1 << lr, sh = row_bits - lr, nbins = W * R;
+  auto bin_of = [&](int p) -> int { return (int)S.scol[p] * R + (int)(key_row(S.sk[p]) >> sh); };
+  for (int b = tid; b < nbins; b += nthr) S.v.bk.cursor[b] = 0u;
+  __syncthreads();
+  for (int p = tid; p < m; p += nthr) atomicAdd(&S.v.bk.cursor[bin_of(p)], 1u);
+  __syncthreads();
+  {
+    constexpr int kPer = kTBins / kSegThreads;
+    const int b0 = tid * kPer;
+    unsigned loc[kPer];
+    long long sum = 0;
+#pragma unroll
+    for (int q = 0; q < kPer; q++) {
+      loc[q] = (b0 + q < nbins) ? S.v.bk.cursor[b0 + q] : 0u;
+      sum += loc[q];
+    }
+    long long tot;
+    long long run = block_exclusive_scan<long long>(sum, S.scan_tmp, &tot);
+#pragma unroll
+    for (int q = 0; q < kPer; q++) {
+      if (b0 + q < nbins) {
+        S.v.bk.bstart[b0 + q] = (unsigned short)run;
+        S.v.bk.cursor[b0 + q] = (unsigned)run;
+      }
+      run += loc[q];
+    }
+    if (tid == 0) S.v.bk.bstart[nbins] = (unsigned short)m;
+  }
+  __syncthreads();
+  for (int p = tid; p < m; p += nthr) {
+    const int b = bin_of(p);
+    const unsigned slot = atomicAdd(&S.v.bk.cursor[b], 1u);
+    S.u.sk2[slot] = S.sk[p];
+    S.perm2[slot] = S.perm[p];
+    S.sbin[slot] = (unsigned short)b;
+  }
+  if (tid == 0) {
+    S.n_med = 0;
+    S.n_big = 0;
+  }
+  for (int l = tid; l <= W; l += nthr) S.cstart[l] = S.v.bk.bstart[l * R];
+  __syncthreads();
+  for (int b = tid; b < nbins; b += nthr) {
+    const int L = S.v.bk.bstart[b + 1] - S.v.bk.bstart[b];
+    if (L > kRankMax && L <= kWarpSortMax) S.med[atomicAdd(&S.n_med, 1)] = (short)b;
+    else if (L > kWarpSortMax) S.big[atomicAdd(&S.n_big, 1)] = (short)b;
+  }
+  for (int q = tid; q < m; q += nthr) {
+    const int b = S.sbin[q];
+    const int s0 = S.v.bk.bstart[b], e0b = S.v.bk.bstart[b + 1];
+    if (e0b - s0 <= kRankMax) {
+      const unsigned long long k = S.u.sk2[q];
+      int r = 0;
+      for (int j = s0; j < e0b; j++) r += (S.u.sk2[j] < k);
+      S.sk[s0 + r] = k;
+      S.perm[s0 + r] = S.perm2[q];
+      S.scol[s0 + r] = (unsigned short)(b / R);
+    }
+  }
+  __syncthreads();
+  const int n_med = S.n_med, n_big = S.n_big;
+  for (int q = warp; q < n_med; q += nwarps) {
+    const int b = S.med[q];
+    const int s0 = S.v.bk.bstart[b], L = S.v.bk.bstart[b + 1] - s0;
+    bitonic_sort<false>(S.u.sk2 + s0, L, lane, 32, S.perm2 + s0);
+    for (int i = lane; i < L; i += 32) {
+      S.sk[s0 + i] = S.u.sk2[s0 + i];
+      S.perm[s0 + i] = S.perm2[s0 + i];
+      S.scol[s0 + i] = (unsigned short)(b / R);
+    }
+  }
+  for (int q = 0; q < n_big; q++) {
+    const int b = S.big[q];
+    const int s0 = S.v.bk.bstart[b], L = S.v.bk.bstart[b + 1] - s0;
+    bitonic_sort<true>(S.u.sk2 + s0, L, tid, nthr, S.perm2 + s0);
+    for (int i = tid; i < L; i += nthr) {
+      S.sk[s0 + i] = S.u.sk2[s0 + i];
+      S.perm[s0 + i] = S.perm2[s0 + i];
+      S.scol[s0 + i] = (unsigned short)(b / R);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+}
+
 template <class T, class S1, class S2>
 __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistArgs<T, S1, S2> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PersistSmem<T>& SM = *reinterpret_cast<PersistSmem<T>*>(smem_raw);
-  SegSmem<T>& S = SM.seg;
+  BTileSmem<T>& S = SM.t;
+  __shared__ long long xscan[kSegThreads / 32 + 1];  // scan scratch outside the phase union
   unsigned gen = 0;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const long long G = gridDim.x, g = blockIdx.x;
-  const long long nb = a.n_bins;
+  const long long ncb = a.n_cb;
+  const int wbits = a.wbits, W = 1 << wbits;
   AS_PHASE_MARK(a, 0);
   a.s1.set_cache(SM.h.colc);
   a.s2.set_cache(SM.h.colc);
 
-  // ---------------- phase 1: histogram ----------------
-  if (a.smem_hist) {
-    for (long long p = g; p < a.P1; p += G) {
-      for (long long b = tid; b < nb; b += nthr) SM.h.hist[b] = 0u;
-      __syncthreads();
-      auto inc = [&](unsigned b, unsigned, unsigned long long, long long) { atomicAdd(&SM.h.hist[b], 1u); };
-      a.s1.visit(p, a.P1, true, inc);
-      a.s2.visit(p, a.P1, true, inc);
-      __syncthreads();
-      unsigned* row = a.partials + p * nb;
-      for (long long b = tid; b < nb; b += nthr) row[b] = SM.h.hist[b];
-      __syncthreads();
-    }
-  } else {
-    auto inc = [&](unsigned b, unsigned, unsigned long long, long long) { atomicAdd(&a.counts[b], 1u); };
+  // ---------------- phase 1: coarse histogram + range reservation ----------------
+  for (long long b = tid; b < ncb; b += nthr) SM.h.a[b] = 0u;
+  __syncthreads();
+  {
+    auto inc = [&](unsigned c, unsigned, unsigned long long, long long) { atomicAdd(&SM.h.a[c >> wbits], 1u); };
     a.s1.visit(g, G, true, inc);
     a.s2.visit(g, G, true, inc);
   }
+  __syncthreads();
+  for (long long b = tid; b < ncb; b += nthr) {
+    const unsigned h = SM.h.a[b];
+    SM.h.b[b] = h ? atomicAdd(&a.cb_cnt[b], h) : 0u;
+    SM.h.a[b] = 0u;
+  }
   grid_sync(a.gb, gen);
   AS_PHASE_MARK(a, gen);
 
-  // ---------------- phase 2: bucket scan ----------------
-  // Smem-histogram path: the partials matrix [P1][nb] is walked in
-  // (256-bucket block) x (range of chunks) work items so every access is
-  // coalesced: 2a range sums, 2b bucket totals + grid-wide scan -> seg_ptr,
-  // 2c per-(chunk, bucket) bases written back into partials.
-  const long long n_bc = (nb + nthr - 1) / nthr;
-  const long long n_pr = a.smem_hist ? max(1ll, min(a.n_pr_max, G / max(1ll, n_bc))) : 1;
-  const long long pr_len = (a.P1 + n_pr - 1) / n_pr;
-  if (a.smem_hist) {
-    for (long long w = g; w < n_bc * n_pr; w += G) {
-      const long long bc = w % n_bc, pr = w / n_bc;
-      const long long b = bc * nthr + tid;
-      if (b < nb) {
-        const long long p0 = pr * pr_len, p1 = min(a.P1, p0 + pr_len);
-        unsigned sacc = 0;
-#pragma unroll 4
-        for (long long p = p0; p < p1; p++) sacc += a.partials[p * nb + b];
-        a.range_sum[pr * nb + b] = sacc;
-      }
-    }
-    grid_sync(a.gb, gen);
-  AS_PHASE_MARK(a, gen);
-  }
-  long long blo, bhi;
-  cta_range(nb, g, G, &blo, &bhi);
+  // ---------------- phase 2: every CTA scans the bucket counts ----------------
   {
     long long running = 0;
-    for (long long cb = blo; cb < bhi; cb += nthr) {
+    for (long long cb = 0; cb < ncb; cb += nthr) {
       const long long b = cb + tid;
-      long long tot = 0;
-      if (b < bhi) {
-        if (a.smem_hist) {
-          for (long long pr = 0; pr < n_pr; pr++) tot += a.range_sum[pr * nb + b];
-        } else {
-          tot = a.counts[b];
-        }
-      }
+      const long long cnt = b < ncb ? (long long)__ldcg(&a.cb_cnt[b]) : 0;
       long long ctot;
-      const long long ex = block_exclusive_scan<long long>(tot, S.scan_tmp, &ctot);
-      if (b < bhi) a.seg_ptr[b] = running + ex;  // CTA-local for now
+      const long long ex = block_exclusive_scan<long long>(cnt, xscan, &ctot);
+      if (b < ncb) {
+        SM.h.b[b] += (unsigned)(running + ex);  // slot base of this CTA's range
+        if (g == 0) a.cb_start[b] = running + ex;
+      }
       running += ctot;
     }
-    if (tid == 0) a.cta_sums[g] = running;
+    if (g == 0 && tid == 0) a.cb_start[ncb] = running;
   }
-  grid_sync(a.gb, gen);
-  AS_PHASE_MARK(a, gen);
-  {
-    long long pre = 0;
-    for (long long q = tid; q < g; q += nthr) pre += a.cta_sums[q];
-    pre = block_reduce_sum<long long>(pre, S.scan_tmp);
-    for (long long b = blo + tid; b < bhi; b += nthr) {
-      const long long start = pre + a.seg_ptr[b];
-      a.seg_ptr[b] = start;
-      long long tot;
-      if (a.smem_hist) {
-        tot = 0;
-        for (long long pr = 0; pr < n_pr; pr++) tot += a.range_sum[pr * nb + b];
-      } else {
-        tot = a.counts[b];
-        a.counts[b] = 0u;
-      }
-      emit_tile_bounds(b, start, start + tot, a.n_tiles, a.tile_c0);
-    }
-    if (g == G - 1 && tid == 0) {
-      long long total = pre + a.cta_sums[g];
-      a.seg_ptr[nb] = total;
-      finish_tile_bounds(nb, total, a.n_tiles, a.tile_c0);
-    }
-  }
-  grid_sync(a.gb, gen);
-  AS_PHASE_MARK(a, gen);
-  if (a.smem_hist) {
-    for (long long w = g; w < n_bc * n_pr; w += G) {
-      const long long bc = w % n_bc, pr = w / n_bc;
-      const long long b = bc * nthr + tid;
-      if (b < nb) {
-        long long run = a.seg_ptr[b];
-        for (long long q = 0; q < pr; q++) run += a.range_sum[q * nb + b];
-        const long long p0 = pr * pr_len, p1 = min(a.P1, p0 + pr_len);
-        for (long long p = p0; p < p1; p++) {
-          const unsigned c = a.partials[p * nb + b];
-          a.partials[p * nb + b] = (unsigned)run;
-          run += c;
-        }
-      }
-    }
-    grid_sync(a.gb, gen);
-  AS_PHASE_MARK(a, gen);
-  }
+  __syncthreads();
 
-  // ---------------- phase 3: scatter keys and values ----------------
-  if (a.smem_hist) {
-    for (long long p = g; p < a.P1; p += G) {
-      const unsigned* row = a.partials + p * nb;
-      for (long long b = tid; b < nb; b += nthr) SM.h.hist[b] = row[b];
-      __syncthreads();
-      a.s1.visit(p, a.P1, false, [&](unsigned b, unsigned minor, unsigned long long idx, long long i) {
-        const unsigned slot = atomicAdd(&SM.h.hist[b], 1u);
-        a.keys[slot] = ((unsigned long long)minor << 32) | idx;
-        a.vals_b[slot] = a.s1.value(i);
-      });
-      a.s2.visit(p, a.P1, false, [&](unsigned b, unsigned minor, unsigned long long idx, long long i) {
-        const unsigned slot = atomicAdd(&SM.h.hist[b], 1u);
-        a.keys[slot] = ((unsigned long long)minor << 32) | idx;
-        a.vals_b[slot] = a.s2.value(i);
-      });
-      __syncthreads();
-    }
-  } else {
-    a.s1.visit(g, G, false, [&](unsigned b, unsigned minor, unsigned long long idx, long long i) {
-      const long long slot = a.seg_ptr[b] + atomicAdd(&a.counts[b], 1u);
-      a.keys[slot] = ((unsigned long long)minor << 32) | idx;
-      a.vals_b[slot] = a.s1.value(i);
-    });
-    a.s2.visit(g, G, false, [&](unsigned b, unsigned minor, unsigned long long idx, long long i) {
-      const long long slot = a.seg_ptr[b] + atomicAdd(&a.counts[b], 1u);
-      a.keys[slot] = ((unsigned long long)minor << 32) | idx;
-      a.vals_b[slot] = a.s2.value(i);
-    });
-  }
+  // ---------------- phase 3: scatter keys, columns and values ----------------
+  a.s1.visit(g, G, false, [&](unsigned c, unsigned minor, unsigned long long idx, long long i) {
+    const unsigned cb = c >> wbits;
+    const unsigned slot = SM.h.b[cb] + atomicAdd(&SM.h.a[cb], 1u);
+    a.keys[slot] = ((unsigned long long)minor << 32) | idx;
+    a.colb[slot] = c;
+    a.vals_b[slot] = a.s1.value(i);
+  });
+  a.s2.visit(g, G, false, [&](unsigned c, unsigned minor, unsigned long long idx, long long i) {
+    const unsigned cb = c >> wbits;
+    const unsigned slot = SM.h.b[cb] + atomicAdd(&SM.h.a[cb], 1u);
+    a.keys[slot] = ((unsigned long long)minor << 32) | idx;
+    a.colb[slot] = c;
+    a.vals_b[slot] = a.s2.value(i);
+  });
   grid_sync(a.gb, gen);
   AS_PHASE_MARK(a, gen);
 
-  // ---------------- phase 4: tiles -> temporaries ----------------
-  SegIn in{a.seg_ptr, nb, a.n_upper, a.keys, a.keys_alt, a.row_bits, a.idx_bits, 0, a.tile_c0};
-  SegOut<T> out{a.col_ptr, a.tmp_rows, a.tmp_vals, a.info, nullptr, a.ticket};
+  // ---------------- phase 4: bucket tiles ----------------
   while (true) {
-    if (tid == 0) S.tile = (long long)atomicAdd(a.ticket, 1u);
+    if (tid == 0) {
+      const long long t = (long long)atomicAdd(a.ticket, 1u);
+      S.tile = t;
+      if (t < ncb) {
+        S.s = __ldcg(&a.cb_start[t]);
+        S.m = __ldcg(&a.cb_start[t + 1]) - S.s;
+      }
+    }
     __syncthreads();
     const long long t = S.tile;
+    if (t >= ncb) break;
+    const long long s = S.s, m = S.m;
+    const unsigned col_base = (unsigned)(t << wbits);
+    const int Wt = (int)min((long long)W, a.n_cols - (long long)col_base);  // columns of this bucket
+    if (m <= kCap) {
+      for (long long i = tid; i < m; i += nthr) {
+        S.sk[i] = a.keys[s + i];
+        S.scol[i] = (unsigned short)(a.colb[s + i] - col_base);
+        S.perm[i] = (unsigned short)i;
+      }
+      __syncthreads();
+      sort_bucket_smem(S, (int)m, W, a.row_bits);
+      bucket_chunk_reduce<T>(S, 0, (int)m, m, nullptr, nullptr, col_base, a.vs, a.mode, a.prune, a.vals_b + s);
+      for (int p = tid; p < m; p += nthr) {
+        const unsigned e0 = S.v.excl[p], e1 = S.v.excl[p + 1];
+        if (e1 != e0) {
+          a.tmp_rows[s + e0] = (int)key_row(S.sk[p]);
+          a.tmp_vals[s + e0] = S.u.rv[p];
+        }
+      }
+      for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = S.v.excl[S.cstart[l + 1]] - S.v.excl[S.cstart[l]];
+    } else {
+      // oversized bucket: radix sort by (column, row, input order) in global memory
+      int shifts[24], nbits[24], fromp[24], np = 0;
+      for (int bb = 0; bb < a.idx_bits; bb += 8) {
+        shifts[np] = bb;
+        nbits[np] = min(8, a.idx_bits - bb);
+        fromp[np] = 0;
+        np++;
+      }
+      for (int bb = 0; bb < a.row_bits; bb += 8) {
+        shifts[np] = 32 + bb;
+        nbits[np] = min(8, a.row_bits - bb);
+        fromp[np] = 0;
+        np++;
+      }
+      for (int bb = 0; bb < wbits; bb += 8) {  // the payload holds the column; bucket-local bits only
+        shifts[np] = bb;
+        nbits[np] = min(8, wbits - bb);
+        fromp[np] = 1;
+        np++;
+      }
+      block_radix_sort_kv(a.keys + s, a.colb + s, a.keys_alt + s, a.colb_alt + s, m, shifts, nbits, fromp, np,
+                          S.u.rs.hist, S.u.rs.wcnt);
+      for (int l = tid; l < Wt; l += nthr) S.ckept[l] = 0u;
+      __syncthreads();
+      long long run_base = 0;
+      for (long long b = 0; b < m; b += kCap) {
+        const int cm = (int)min((long long)kCap, m - b);
+        for (int i = tid; i < cm; i += nthr) {
+          S.sk[i] = a.keys[s + b + i];
+          S.scol[i] = (unsigned short)(a.colb[s + b + i] - col_base);
+        }
+        __syncthreads();
+        const long long ctot = bucket_chunk_reduce<T>(S, b, cm, m, a.keys + s, a.colb + s, col_base, a.vs, a.mode,
+                                                      a.prune, nullptr);
+        for (int p = tid; p < cm; p += nthr) {
+          const unsigned e0 = S.v.excl[p], e1 = S.v.excl[p + 1];
+          if (e1 != e0) {
+            a.tmp_rows[s + run_base + e0] = (int)key_row(S.sk[p]);
+            a.tmp_vals[s + run_base + e0] = S.u.rv[p];
+            atomicAdd(&S.ckept[S.scol[p]], 1u);
+          }
+        }
+        run_base += ctot;
+        __syncthreads();
+      }
+      for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = S.ckept[l];
+    }
     __syncthreads();
-    if (t >= a.n_tiles) break;
-    process_tile<true, T>(S, in, a.vs, a.mode, a.prune, out, t, a.n_tiles, a.vals_b, a.tile_total);
   }
   grid_sync(a.gb, gen);
   AS_PHASE_MARK(a, gen);
 
-  // ---------------- phase 5: tile prefixes, placement ----------------
-  long long tlo, thi;
-  cta_range(a.n_tiles, g, G, &tlo, &thi);
+  // ---------------- phase 5: column scan and placement ----------------
+  long long clo, chi;
+  cta_range(a.n_cols, g, G, &clo, &chi);
   {
-    long long s = 0;
-    for (long long t = tlo + tid; t < thi; t += nthr) s += a.tile_total[t];
-    s = block_reduce_sum<long long>(s, S.scan_tmp);
-    if (tid == 0) a.cta_sums[G + g] = s;
+    long long sum = 0;
+    for (long long c = clo + tid; c < chi; c += nthr) sum += __ldcg(&a.col_kept[c]);
+    sum = block_reduce_sum<long long>(sum, xscan);
+    if (tid == 0) a.cta_sums[g] = sum;
   }
   grid_sync(a.gb, gen);
   AS_PHASE_MARK(a, gen);
   {
     long long pre = 0;
-    for (long long q = tid; q < g; q += nthr) pre += a.cta_sums[G + q];
-    pre = block_reduce_sum<long long>(pre, S.scan_tmp);
-    for (long long t = tlo; t < thi; t++) {  // block-uniform
-      const long long c0 = a.tile_c0[t], c1 = a.tile_c0[t + 1];
-      const long long e0 = a.seg_ptr[c0];
-      const long long cnt = a.tile_total[t];
-      for (long long i = tid; i < cnt; i += nthr) {
-        a.row_idx[pre + i] = a.tmp_rows[e0 + i];
-        a.out_vals[pre + i] = a.tmp_vals[e0 + i];
-      }
-      for (long long c = c0 + tid; c < c1; c += nthr) a.col_ptr[c] += (int)pre;
-      pre += cnt;
+    for (long long q = tid; q < g; q += nthr) pre += __ldcg(&a.cta_sums[q]);
+    pre = block_reduce_sum<long long>(pre, xscan);
+    long long running = pre;
+    for (long long cb = clo; cb < chi; cb += nthr) {
+      const long long c = cb + tid;
+      const long long k = c < chi ? (long long)__ldcg(&a.col_kept[c]) : 0;
+      long long ctot;
+      const long long ex = block_exclusive_scan<long long>(k, xscan, &ctot);
+      if (c < chi) a.col_ptr[c] = (int)(running + ex);
+      running += ctot;
     }
     if (g == G - 1 && tid == 0) {
-      a.col_ptr[nb] = (int)pre;
-      a.info[0] = pre;
+      a.col_ptr[a.n_cols] = (int)running;
+      a.info[0] = running;
+    }
+  }
+  grid_sync(a.gb, gen);
+  AS_PHASE_MARK(a, gen);
+  for (long long t = g; t < ncb; t += G) {
+    const long long c0 = t << wbits;
+    const long long c1 = min(a.n_cols, c0 + W);
+    const long long dst = __ldcg(&a.col_ptr[c0]);
+    const long long cnt = __ldcg(&a.col_ptr[c1]) - dst;
+    const long long src = __ldcg(&a.cb_start[t]);
+    for (long long i = tid; i < cnt; i += nthr) {
+      a.row_idx[dst + i] = __ldcg(&a.tmp_rows[src + i]);
+      a.out_vals[dst + i] = __ldcg(&a.tmp_vals[src + i]);
     }
   }
   __syncthreads();
