@@ -210,6 +210,7 @@ struct PersistArgs {
   unsigned* ticket;
   GridBar gb;
   unsigned long long* phase_ts;  // optional: globaltimer after each phase (debug)
+  const long long* pre_ptr;      // non-null: input already bucketed by column (SpGEMM products)
 };
 
 template <class T>
@@ -240,6 +241,7 @@ struct BTileSmem {
   int n_med, n_big;
   long long scan_tmp[kSegThreads / 32 + 1];
   unsigned ckept[kMaxW];  // kept per column (oversized path)
+  unsigned obin[2 * kTBins + 1];  // bin starts of an oversized bucket's split
   long long tile, s, m;
 };
 
@@ -262,7 +264,7 @@ AS_DEVICE_INLINE void cta_range(long long n, long long g, long long G, long long
 // Block-level stable LSD radix sort of (u64 key, u32 payload) pairs in global
 // memory; pass i sorts by bits [shift, shift+nbits) of the key (from_payload
 // = 0) or of the payload (1).  Leaves the result in (k, p).
-__device__ void block_radix_sort_kv(unsigned long long* k, unsigned* p, unsigned long long* k_alt, unsigned* p_alt,
+static __device__ void block_radix_sort_kv(unsigned long long* k, unsigned* p, unsigned long long* k_alt, unsigned* p_alt,
                                     long long L, const int* shifts, const int* nbits, const int* from_payload,
                                     int npass, unsigned* hist, unsigned* wcnt) {
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -504,6 +506,162 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int W, int row_bits) {
   __syncthreads();
 }
 
+// A bucket larger than the tile: split it in global memory into bins of
+// (column, high row bits) -- every (column, row) run stays inside one bin --
+// then process consecutive bins in groups that fit the tile with the shared-
+// memory sort; a single bin still larger than the tile is radix-sorted in
+// global memory and streamed.  Values are read by input index.
+template <class T, class S1, class S2>
+__device__ void process_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a, long long s, long long m,
+                                         unsigned col_base, int wbits, int Wt) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int W = 1 << wbits;
+  unsigned* bstart = S.obin;  // nbins + 1 u32 bin starts (bucket-relative)
+  unsigned* cursor = reinterpret_cast<unsigned*>(&S.u) + kMaxW;  // [<= 2 * kTBins] (S.u is free here)
+  unsigned long long* gk = a.keys + s;
+  unsigned* gc = a.colb + s;
+  unsigned long long* ak = a.keys_alt + s;
+  unsigned* ac = a.colb_alt + s;
+  // per-column row split sized from the column's count: column l gets
+  // 2^lr[l] bins of ~`target` keys, so one heavy column does not overflow
+  // the tile (bins of one (column, row prefix) still keep every run whole)
+  unsigned* ccount = reinterpret_cast<unsigned*>(&S.u);  // [W] column counts
+  unsigned short* bbase = S.scol;          // [W+1] first bin of each column
+  unsigned short* clr = S.perm;            // [W]  row-prefix bits per column
+  for (int l = tid; l < W; l += nthr) ccount[l] = 0u;
+  for (int l = tid; l < Wt; l += nthr) S.ckept[l] = 0u;
+  __syncthreads();
+  for (long long i = tid; i < m; i += nthr) atomicAdd(&ccount[gc[i] - col_base], 1u);
+  __syncthreads();
+  // sum_l 2^lr[l] <= W + 2m/target <= 2*kTBins bins
+  const unsigned target = (unsigned)max(1024ll, (2 * m + (2 * kTBins - W) - 1) / (2 * kTBins - W));
+  if (tid < 32) {
+    unsigned carry = 0;
+    for (int l0 = 0; l0 < W; l0 += 32) {
+      const int l = l0 + tid;
+      int lr = 0;
+      if (l < W)
+        while (lr < a.row_bits && (ccount[l] >> lr) > target) lr++;
+      const unsigned nb = l < W ? (1u << lr) : 0u;
+      const unsigned inc = warp_inclusive_scan(nb);
+      if (l < W) {
+        bbase[l] = (unsigned short)(carry + inc - nb);
+        clr[l] = (unsigned short)lr;
+      }
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (tid == 0) bbase[W] = (unsigned short)carry;
+  }
+  __syncthreads();
+  const int nbins = bbase[W];
+  auto bin_of = [&](unsigned long long k, unsigned c) -> int {
+    const int l = (int)(c - col_base);
+    return (int)bbase[l] + (int)(key_row(k) >> (a.row_bits - clr[l]));
+  };
+  for (int b = tid; b < nbins; b += nthr) cursor[b] = 0u;
+  __syncthreads();
+  for (long long i = tid; i < m; i += nthr) atomicAdd(&cursor[bin_of(gk[i], gc[i])], 1u);
+  __syncthreads();
+  if (tid < 32) {
+    unsigned carry = 0;
+    for (int b0 = 0; b0 < nbins; b0 += 32) {
+      const unsigned v = (b0 + tid < nbins) ? cursor[b0 + tid] : 0u;
+      const unsigned inc = warp_inclusive_scan(v);
+      if (b0 + tid < nbins) {
+        bstart[b0 + tid] = carry + inc - v;
+        cursor[b0 + tid] = carry + inc - v;
+      }
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (tid == 0) bstart[nbins] = carry;
+  }
+  __syncthreads();
+  for (long long i = tid; i < m; i += nthr) {
+    const unsigned long long k = gk[i];
+    const unsigned c = gc[i];
+    const unsigned pos = atomicAdd(&cursor[bin_of(k, c)], 1u);
+    ak[pos] = k;
+    ac[pos] = c;
+  }
+  __syncthreads();
+  long long run_base = 0;
+  int b0 = 0;
+  while (b0 < nbins) {  // block-uniform walk over groups of bins
+    int b1 = b0 + 1;
+    while (b1 < nbins && bstart[b1 + 1] - bstart[b0] <= (unsigned)kCap) b1++;
+    const long long e0 = bstart[b0], L = (long long)bstart[b1] - e0;
+    if (L > 0 && L <= kCap) {
+      for (int i = tid; i < L; i += nthr) {
+        S.sk[i] = ak[e0 + i];
+        S.scol[i] = (unsigned short)(ac[e0 + i] - col_base);
+        S.perm[i] = (unsigned short)i;
+      }
+      __syncthreads();
+      sort_bucket_smem(S, (int)L, W, a.row_bits);
+      const long long ctot = bucket_chunk_reduce<T>(S, 0, (int)L, L, nullptr, nullptr, col_base, a.vs, a.mode,
+                                                    a.prune, nullptr);
+      for (int p = tid; p < L; p += nthr) {
+        const unsigned x0 = S.v.excl[p], x1 = S.v.excl[p + 1];
+        if (x1 != x0) {
+          a.tmp_rows[s + run_base + x0] = (int)key_row(S.sk[p]);
+          a.tmp_vals[s + run_base + x0] = S.u.rv[p];
+          atomicAdd(&S.ckept[S.scol[p]], 1u);
+        }
+      }
+      run_base += ctot;
+      __syncthreads();
+    } else if (L > kCap) {  // one bin above the tile: global radix sort, streamed reduce
+      int shifts[24], nbits[24], fromp[24], np = 0;
+      for (int bb = 0; bb < a.idx_bits; bb += 8) {
+        shifts[np] = bb;
+        nbits[np] = min(8, a.idx_bits - bb);
+        fromp[np] = 0;
+        np++;
+      }
+      for (int bb = 0; bb < a.row_bits; bb += 8) {
+        shifts[np] = 32 + bb;
+        nbits[np] = min(8, a.row_bits - bb);
+        fromp[np] = 0;
+        np++;
+      }
+      for (int bb = 0; bb < wbits; bb += 8) {
+        shifts[np] = bb;
+        nbits[np] = min(8, wbits - bb);
+        fromp[np] = 1;
+        np++;
+      }
+      __syncthreads();
+      block_radix_sort_kv(ak + e0, ac + e0, gk + e0, gc + e0, L, shifts, nbits, fromp, np, S.u.rs.hist,
+                          S.u.rs.wcnt);
+      unsigned long long* bk2 = ak + e0;
+      unsigned* bc2 = ac + e0;
+      for (long long b = 0; b < L; b += kCap) {
+        const int cm = (int)min((long long)kCap, L - b);
+        for (int i = tid; i < cm; i += nthr) {
+          S.sk[i] = bk2[b + i];
+          S.scol[i] = (unsigned short)(bc2[b + i] - col_base);
+        }
+        __syncthreads();
+        const long long ctot = bucket_chunk_reduce<T>(S, b, cm, L, bk2, bc2, col_base, a.vs, a.mode, a.prune,
+                                                      nullptr);
+        for (int p = tid; p < cm; p += nthr) {
+          const unsigned x0 = S.v.excl[p], x1 = S.v.excl[p + 1];
+          if (x1 != x0) {
+            a.tmp_rows[s + run_base + x0] = (int)key_row(S.sk[p]);
+            a.tmp_vals[s + run_base + x0] = S.u.rv[p];
+            atomicAdd(&S.ckept[S.scol[p]], 1u);
+          }
+        }
+        run_base += ctot;
+        __syncthreads();
+      }
+    }
+    b0 = b1;
+  }
+  for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = S.ckept[l];
+  __syncthreads();
+}
+
 template <class T, class S1, class S2>
 __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistArgs<T, S1, S2> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -519,6 +677,13 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
   a.s1.set_cache(SM.h.colc);
   a.s2.set_cache(SM.h.colc);
 
+  if (a.pre_ptr != nullptr) {
+    // pre-bucketed input (SpGEMM products): keys / colb / vals_b already sit
+    // in output-column order; only the coarse bucket starts are needed
+    for (long long t = g * nthr + tid; t <= ncb; t += G * nthr) a.cb_start[t] = a.pre_ptr[min(t << wbits, a.n_cols)];
+    grid_sync(a.gb, gen);
+    AS_PHASE_MARK(a, gen);
+  } else {
   // ---------------- phase 1: coarse histogram + range reservation ----------------
   for (long long b = tid; b < ncb; b += nthr) SM.h.a[b] = 0u;
   __syncthreads();
@@ -571,6 +736,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
   });
   grid_sync(a.gb, gen);
   AS_PHASE_MARK(a, gen);
+  }
 
   // ---------------- phase 4: bucket tiles ----------------
   while (true) {
@@ -606,52 +772,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
       }
       for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = S.v.excl[S.cstart[l + 1]] - S.v.excl[S.cstart[l]];
     } else {
-      // oversized bucket: radix sort by (column, row, input order) in global memory
-      int shifts[24], nbits[24], fromp[24], np = 0;
-      for (int bb = 0; bb < a.idx_bits; bb += 8) {
-        shifts[np] = bb;
-        nbits[np] = min(8, a.idx_bits - bb);
-        fromp[np] = 0;
-        np++;
-      }
-      for (int bb = 0; bb < a.row_bits; bb += 8) {
-        shifts[np] = 32 + bb;
-        nbits[np] = min(8, a.row_bits - bb);
-        fromp[np] = 0;
-        np++;
-      }
-      for (int bb = 0; bb < wbits; bb += 8) {  // the payload holds the column; bucket-local bits only
-        shifts[np] = bb;
-        nbits[np] = min(8, wbits - bb);
-        fromp[np] = 1;
-        np++;
-      }
-      block_radix_sort_kv(a.keys + s, a.colb + s, a.keys_alt + s, a.colb_alt + s, m, shifts, nbits, fromp, np,
-                          S.u.rs.hist, S.u.rs.wcnt);
-      for (int l = tid; l < Wt; l += nthr) S.ckept[l] = 0u;
-      __syncthreads();
-      long long run_base = 0;
-      for (long long b = 0; b < m; b += kCap) {
-        const int cm = (int)min((long long)kCap, m - b);
-        for (int i = tid; i < cm; i += nthr) {
-          S.sk[i] = a.keys[s + b + i];
-          S.scol[i] = (unsigned short)(a.colb[s + b + i] - col_base);
-        }
-        __syncthreads();
-        const long long ctot = bucket_chunk_reduce<T>(S, b, cm, m, a.keys + s, a.colb + s, col_base, a.vs, a.mode,
-                                                      a.prune, nullptr);
-        for (int p = tid; p < cm; p += nthr) {
-          const unsigned e0 = S.v.excl[p], e1 = S.v.excl[p + 1];
-          if (e1 != e0) {
-            a.tmp_rows[s + run_base + e0] = (int)key_row(S.sk[p]);
-            a.tmp_vals[s + run_base + e0] = S.u.rv[p];
-            atomicAdd(&S.ckept[S.scol[p]], 1u);
-          }
-        }
-        run_base += ctot;
-        __syncthreads();
-      }
-      for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = S.ckept[l];
+      process_oversized_bucket<T>(S, a, s, m, col_base, wbits, Wt);
     }
     __syncthreads();
   }

@@ -1,0 +1,169 @@
+// persist_host.cuh -- host side of the persistent bucket-sort kernel:
+// workspace carving, coarse-bucket sizing, cooperative launch.
+#pragma once
+
+#include <stdlib.h>
+
+#include "capi_util.cuh"
+#include "persist.cuh"
+
+namespace as {
+
+constexpr long long kMaxDim = 0x7fffffffll;
+constexpr long long kMaxGrid = 148 * 8;  // upper bound of the co-resident grid
+
+struct PersistWs {
+  unsigned* zero;  // [0] ticket, [16] barrier arrive, [32] barrier generation, then cb_cnt
+  unsigned* cb_cnt;
+  size_t zero_bytes;
+  long long* cb_start;
+  unsigned long long* keys;
+  unsigned long long* keys_alt;
+  unsigned* colb;
+  unsigned* colb_alt;
+  void* vals_b;
+  int* tmp_rows;
+  void* tmp_vals;
+  unsigned* col_kept;
+  long long* cta_sums;
+  long long* own_info;
+  int wbits;
+  long long n_cb;
+};
+
+// Coarse buckets of W = 2^wbits output columns: ~0.8 * kCap elements per
+// bucket on average, at most kMaxCoarse buckets.  Returns -1 when the column
+// count exceeds kMaxCoarse * kMaxW.
+static inline int choose_wbits(long long n, long long n_cols) {
+  const double avg = n_cols > 0 ? (double)n / (double)n_cols : 0.0;
+  int wb = 0;
+  while ((1 << (wb + 1)) <= kMaxW && (double)(1 << (wb + 1)) * avg <= 0.8 * kCap) wb++;
+  while (wb <= 10 && ((n_cols + (1ll << wb) - 1) >> wb) > kMaxCoarse) wb++;
+  return ((n_cols + (1ll << wb) - 1) >> wb) > kMaxCoarse || (1 << wb) > kMaxW ? -1 : wb;
+}
+
+static size_t carve_persist(Carve& c, PersistWs* w, long long n, long long n_cols, size_t val_bytes) {
+  w->wbits = choose_wbits(n, n_cols);
+  const int wb = w->wbits < 0 ? 10 : w->wbits;
+  w->n_cb = (n_cols + (1ll << wb) - 1) >> wb;
+  w->zero = c.take<unsigned>(64);
+  w->cb_cnt = c.take<unsigned>(std::max(1ll, w->n_cb));
+  w->zero_bytes = c.off;
+  w->cb_start = c.take<long long>(w->n_cb + 1);
+  const long long n1 = std::max(1ll, n);
+  w->keys = c.take<unsigned long long>(n1);
+  w->keys_alt = c.take<unsigned long long>(n1);
+  w->colb = c.take<unsigned>(n1);
+  w->colb_alt = c.take<unsigned>(n1);
+  w->vals_b = (void*)c.take<char>(n1 * val_bytes);
+  w->tmp_rows = c.take<int>(n1);
+  w->tmp_vals = (void*)c.take<char>(n1 * val_bytes);
+  w->col_kept = c.take<unsigned>(std::max(1ll, n_cols));
+  w->cta_sums = c.take<long long>(kMaxGrid);
+  w->own_info = c.take<long long>(2);
+  return c.off;
+}
+
+template <class T, class S1, class S2>
+static int launch_persist(PersistArgs<T, S1, S2>& a, cudaStream_t st) {
+  static int grid = 0;
+  const size_t smem = sizeof(PersistSmem<T>);
+  auto kern = persist_bucket_kernel<T, S1, S2>;
+  if (grid == 0) {
+    AS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0, dev = 0, sms = 0;
+    AS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSegThreads, smem));
+    AS_CUDA_TRY(cudaGetDevice(&dev));
+    AS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    AS_REQUIRE(per_sm > 0, AS_ERR_CUDA, "persistent kernel does not fit on an SM");
+    grid = (int)std::min<long long>((long long)per_sm * sms, kMaxGrid);
+  }
+  void* args[] = {(void*)&a};
+  AS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSegThreads), args, smem, st));
+  return AS_OK;
+}
+
+// Launch the persistent kernel on an already carved workspace.  pre_ptr !=
+// nullptr: w.keys / w.colb / w.vals_b already hold the input bucketed by
+// output column (pre_ptr = its column pointer, n elements).
+template <class T, class S1, class S2>
+static int run_persist_ws(PersistWs& w, const S1& s1, const S2& s2, long long n, long long n_cols, int row_bits,
+                          int mode, int prune, ValSrc<T> vs, int* col_ptr, int* row_idx, T* out_vals,
+                          long long* info, bool init_info, const long long* pre_ptr, cudaStream_t st) {
+  AS_REQUIRE(w.wbits >= 0, AS_ERR_ARG, "%lld output columns exceed the %lld supported by the bucket kernel",
+             n_cols, (long long)kMaxCoarse * kMaxW);
+  if (info == nullptr) info = w.own_info;
+  AS_CUDA_TRY(cudaMemsetAsync(w.zero, 0, w.zero_bytes, st));
+  if (init_info) AS_CUDA_TRY(cudaMemsetAsync(info, 0x7f, 2 * sizeof(long long), st));
+  PersistArgs<T, S1, S2> a;
+  a.s1 = s1;
+  a.s2 = s2;
+  a.n_cols = n_cols;
+  a.n_upper = n;
+  a.wbits = w.wbits;
+  a.n_cb = w.n_cb;
+  a.cb_cnt = w.cb_cnt;
+  a.cb_start = w.cb_start;
+  a.keys = w.keys;
+  a.keys_alt = w.keys_alt;
+  a.colb = w.colb;
+  a.colb_alt = w.colb_alt;
+  a.vals_b = (T*)w.vals_b;
+  a.tmp_rows = w.tmp_rows;
+  a.tmp_vals = (T*)w.tmp_vals;
+  a.col_kept = w.col_kept;
+  a.cta_sums = w.cta_sums;
+  a.row_bits = row_bits;
+  a.idx_bits = bits_for(n > 0 ? n - 1 : 0);
+  a.mode = mode;
+  a.prune = prune;
+  a.vs = vs;
+  a.col_ptr = col_ptr;
+  a.row_idx = row_idx;
+  a.out_vals = out_vals;
+  a.info = info;
+  a.ticket = w.zero;
+  a.gb = GridBar{w.zero + 16, w.zero + 32};
+  a.phase_ts = nullptr;
+  a.pre_ptr = pre_ptr;
+  static unsigned long long* dbg_ts = nullptr;
+  const bool phase_dbg = getenv("AS_PHASE_TIMES") != nullptr;
+  if (phase_dbg) {
+    if (!dbg_ts) AS_CUDA_TRY(cudaMalloc(&dbg_ts, 16 * sizeof(unsigned long long)));
+    AS_CUDA_TRY(cudaMemsetAsync(dbg_ts, 0, 16 * sizeof(unsigned long long), st));
+    a.phase_ts = dbg_ts;
+  }
+  const int rc = launch_persist<T, S1, S2>(a, st);
+  if (phase_dbg && rc == AS_OK) {
+    unsigned long long h[16];
+    AS_CUDA_TRY(cudaMemcpyAsync(h, dbg_ts, sizeof(h), cudaMemcpyDeviceToHost, st));
+    AS_CUDA_TRY(cudaStreamSynchronize(st));
+    fprintf(stderr, "[phases n=%lld n_cols=%lld W=%d n_cb=%lld]", n, n_cols, 1 << w.wbits, w.n_cb);
+    for (int i = 1; i < 16 && h[i]; i++) fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
+    fprintf(stderr, " us\n");
+  }
+  return rc;
+}
+
+template <class T, class S1, class S2>
+static int run_persist(const S1& s1, const S2& s2, long long n_cols, int row_bits, int mode, int prune, ValSrc<T> vs,
+                       int* col_ptr, int* row_idx, T* out_vals, long long* info, bool init_info, void* ws,
+                       size_t ws_bytes, cudaStream_t st) {
+  const long long n = s1.size() + s2.size();
+  Carve c(ws, ws_bytes);
+  PersistWs w;
+  carve_persist(c, &w, n, n_cols, sizeof(T));
+  AS_REQUIRE(c.ok, AS_ERR_ARG, "workspace too small: %zu < %zu", ws_bytes, c.off);
+  return run_persist_ws<T>(w, s1, s2, n, n_cols, row_bits, mode, prune, vs, col_ptr, row_idx, out_vals, info,
+                           init_info, nullptr, st);
+}
+
+inline size_t persist_ws_bytes(long long n, long long n_cols, size_t val_bytes) {
+  Carve c(nullptr, 0);
+  PersistWs w;
+  carve_persist(c, &w, n, n_cols, val_bytes);
+  return c.off;
+}
+
+
+}  // namespace as

@@ -19,7 +19,7 @@
 //     overflow shared memory are radix-sorted by row bits only, since they
 //     arrive already in index order.
 #include "capi_util.cuh"
-#include "segsort.cuh"
+#include "persist_host.cuh"
 
 namespace as {
 
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kGThreads)
 spgemm_expand_kernel(long long n_cols_b, const int* __restrict__ a_ptr, const int* __restrict__ a_rows,
                      const double* __restrict__ a_vals, const int* __restrict__ b_ptr, const int* __restrict__ b_rows,
                      const double* __restrict__ b_vals, const long long* __restrict__ prod_ptr,
-                     unsigned long long* __restrict__ keys, double* __restrict__ pvals) {
+                     unsigned long long* __restrict__ keys, unsigned* __restrict__ colb, double* __restrict__ pvals) {
   __shared__ int s_off[kGThreads / 32][33];
   __shared__ int s_k[kGThreads / 32][32];
   __shared__ double s_b[kGThreads / 32][32];
@@ -84,6 +84,7 @@ spgemm_expand_kernel(long long n_cols_b, const int* __restrict__ a_ptr, const in
         const int ii = s_k[wib][lo] + (q - s_off[wib][lo]);
         const long long pos = out + q;
         keys[pos] = ((unsigned long long)(unsigned)a_rows[ii] << 32) | (unsigned long long)pos;
+        colb[pos] = (unsigned)j;
         pvals[pos] = __dmul_rn(a_vals[ii], s_b[wib][lo]);
       }
       out += total;
@@ -134,15 +135,7 @@ int as_spgemm_products(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, cons
 }
 
 size_t as_spgemm_workspace_bytes(int64_t n_cols_b, int64_t total_products) {
-  (void)n_cols_b;
-  Carve c(nullptr, 0);
-  c.take<unsigned>(64);
-  c.take<unsigned long long>(seg_engine_tiles(total_products));
-  c.take<long long>(seg_engine_tiles(total_products) + 1);
-  c.take<unsigned long long>(total_products > 0 ? total_products : 1);
-  c.take<unsigned long long>(total_products > 0 ? total_products : 1);
-  c.take<double>(total_products > 0 ? total_products : 1);
-  return c.off;
+  return persist_ws_bytes(total_products, n_cols_b, sizeof(double));
 }
 
 int as_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int32_t* a_col_ptr,
@@ -152,31 +145,22 @@ int as_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int
   cudaStream_t st = S(stream);
   AS_REQUIRE(n_rows_a >= 0 && n_inner >= 0 && n_cols_b >= 0, AS_ERR_SHAPE, "negative dimension");
   AS_REQUIRE(n_rows_a <= 0x7fffffffll && n_cols_b <= 0x7fffffffll, AS_ERR_SHAPE, "dimension outside int32 range");
-  AS_REQUIRE(total_products >= 0 && total_products < 0xffffffffll, AS_ERR_ARG,
-             "%lld products exceed the 32-bit product index", (long long)total_products);
-  AS_REQUIRE(ws_bytes >= as_spgemm_workspace_bytes(n_cols_b, total_products), AS_ERR_ARG, "workspace too small");
+  AS_REQUIRE(total_products >= 0 && total_products <= 0x7fffffffll, AS_ERR_ARG,
+             "%lld products exceed the 31-bit product index", (long long)total_products);
   Carve c(ws, ws_bytes);
-  unsigned* ticket = c.take<unsigned>(64);
-  unsigned long long* states = c.take<unsigned long long>(seg_engine_tiles(total_products));
-  const size_t zero_bytes = c.off;
-  const long long n_tiles = seg_engine_tiles(total_products);
-  long long* tile_c0 = c.take<long long>(n_tiles + 1);
-  unsigned long long* keys = c.take<unsigned long long>(total_products > 0 ? total_products : 1);
-  unsigned long long* keys_alt = c.take<unsigned long long>(total_products > 0 ? total_products : 1);
-  double* pvals = c.take<double>(total_products > 0 ? total_products : 1);
-  AS_CUDA_TRY(cudaMemsetAsync(ws, 0, zero_bytes, st));
+  PersistWs w;
+  carve_persist(c, &w, total_products, n_cols_b, sizeof(double));
+  AS_REQUIRE(c.ok, AS_ERR_ARG, "workspace too small: %zu < %zu", ws_bytes, c.off);
   if (n_cols_b > 0 && total_products > 0) {
     spgemm_expand_kernel<<<grid_for(n_cols_b * 32, kGThreads, 16), kGThreads, 0, st>>>(
-        n_cols_b, a_col_ptr, a_row_idx, a_vals, b_col_ptr, b_row_idx, b_vals, (const long long*)prod_ptr, keys, pvals);
+        n_cols_b, a_col_ptr, a_row_idx, a_vals, b_col_ptr, b_row_idx, b_vals, (const long long*)prod_ptr, w.keys,
+        w.colb, (double*)w.vals_b);
     AS_LAUNCH_CHECK();
   }
-  tile_bounds_kernel<<<grid_for(n_cols_b, 256), 256, 0, st>>>((const long long*)prod_ptr, n_cols_b, n_tiles, tile_c0);
-  AS_LAUNCH_CHECK();
-  ValSrc<double> vs{pvals, nullptr, (unsigned long long)total_products};
-  return launch_seg_engine<double>((const long long*)prod_ptr, tile_c0, n_cols_b, total_products, keys, keys_alt,
-                                   bits_for(n_rows_a > 0 ? n_rows_a - 1 : 0),
-                                   bits_for(total_products > 0 ? total_products - 1 : 0), 1, vs, kSumSeq, 1, col_ptr,
-                                   row_idx, out_vals, (long long*)info, states, ticket, st);
+  ValSrc<double> vs{(const double*)w.vals_b, nullptr, (unsigned long long)total_products};
+  return run_persist_ws<double>(w, NoSrc<double>{}, NoSrc<double>{}, total_products, n_cols_b,
+                                bits_for(n_rows_a > 0 ? n_rows_a - 1 : 0), kSumSeq, 1, vs, col_ptr, row_idx, out_vals,
+                                (long long*)info, false, (const long long*)prod_ptr, st);
 }
 
 }  // extern "C"
