@@ -111,10 +111,10 @@ size_t as_spgemm_products_workspace_bytes(int64_t n_cols_b);
 int as_spgemm_products(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int32_t *a_col_ptr,
                        const int32_t *b_col_ptr, const int32_t *b_row_idx, int64_t *prod_ptr, int64_t *info,
                        void *ws, size_t ws_bytes, void *stream);
-size_t as_spgemm_workspace_bytes(int64_t n_cols_b, int64_t total_products);
+size_t as_spgemm_workspace_bytes(int64_t n_cols_b, int64_t nnz_b, int64_t total_products);
 int as_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int32_t *a_col_ptr,
                   const int32_t *a_row_idx, const double *a_vals, const int32_t *b_col_ptr,
-                  const int32_t *b_row_idx, const double *b_vals, const int64_t *prod_ptr,
+                  const int32_t *b_row_idx, const double *b_vals, int64_t nnz_b, const int64_t *prod_ptr,
                   int64_t total_products, int32_t *col_ptr, int32_t *row_idx, double *out_vals,
                   int64_t *info, void *ws, size_t ws_bytes, void *stream);
 

@@ -142,10 +142,11 @@ def spgemm(n_rows_a, n_inner, n_cols_b, a, b):
     row_idx = torch.empty(cap, dtype=torch.int32, device=dev)
     out_vals = torch.empty(cap, dtype=torch.float64, device=dev)
     info = torch.zeros(2, dtype=torch.int64, device=dev)
-    ws_bytes = L.as_spgemm_workspace_bytes(n_cols_b, total)
+    nnz_b = int(b_rows.numel())
+    ws_bytes = L.as_spgemm_workspace_bytes(n_cols_b, nnz_b, total)
     ws = workspace(ws_bytes, dev)
     check(L.as_spgemm_f64(n_rows_a, n_inner, n_cols_b, ptr(a_ptr), ptr(a_rows), ptr(a_vals), ptr(b_ptr), ptr(b_rows),
-                          ptr(b_vals), ptr(prod_ptr), total, ptr(col_ptr), ptr(row_idx), ptr(out_vals), ptr(info),
+                          ptr(b_vals), nnz_b, ptr(prod_ptr), total, ptr(col_ptr), ptr(row_idx), ptr(out_vals), ptr(info),
                           ptr(ws), ws_bytes, stream()))
     nnz = int(info[0].item())
     return col_ptr, row_idx[:nnz], out_vals[:nnz]

@@ -40,8 +40,8 @@ SIGNATURES = {
     "as_csc_add_f64": (INT, [I64, I64, DBL, DBL, P, P, P, P, P, P, I64, I64, P, P, P, P, P, SZ, P]),
     "as_spgemm_products_workspace_bytes": (SZ, [I64]),
     "as_spgemm_products": (INT, [I64, I64, I64, P, P, P, P, P, P, SZ, P]),
-    "as_spgemm_workspace_bytes": (SZ, [I64, I64]),
-    "as_spgemm_f64": (INT, [I64, I64, I64, P, P, P, P, P, P, P, I64, P, P, P, P, P, SZ, P]),
+    "as_spgemm_workspace_bytes": (SZ, [I64, I64, I64]),
+    "as_spgemm_f64": (INT, [I64, I64, I64, P, P, P, P, P, P, I64, P, I64, P, P, P, P, P, SZ, P]),
     "as_spmm_workspace_bytes": (SZ, [I64, I64, INT]),
     "as_spmm_csr_f32": (INT, [I64, I64, I64, P, P, P, P, I64, P, I64, INT, P, SZ, P]),
     "as_spmm_csr_f64": (INT, [I64, I64, I64, P, P, P, P, I64, P, I64, P, SZ, P]),

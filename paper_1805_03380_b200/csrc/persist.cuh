@@ -211,7 +211,19 @@ struct PersistArgs {
   GridBar gb;
   unsigned long long* phase_ts;  // optional: globaltimer after each phase (debug)
   const long long* pre_ptr;      // non-null: input already bucketed by column (SpGEMM products)
+  // pre_ptr only: variable-width buckets -- bucket t spans columns
+  // [cb_col[t], cb_col[t+1]); tiles are taken in `order` (oversized first)
+  unsigned* cb_col;              // [n_cb + 1]
+  unsigned* order;               // [n_cb]
 };
+
+// Variable-width buckets of pre-bucketed input: column c weighs
+// len(c) + kPreColCost, bucket t holds the columns whose cumulative weight
+// starts in [t * kPreT, (t+1) * kPreT) -- at most kPreT / kPreColCost columns
+// and kPreT elements plus the length of its last column.
+constexpr long long kPreT = 1536;
+constexpr long long kPreColCost = 2;
+static_assert(kPreT / kPreColCost + 1 <= kMaxW, "variable bucket wider than a tile");
 
 template <class T>
 struct BTileSmem {
@@ -242,7 +254,9 @@ struct BTileSmem {
   long long scan_tmp[kSegThreads / 32 + 1];
   unsigned ckept[kMaxW];  // kept per column (oversized path)
   unsigned obin[2 * kTBins + 1];  // bin starts of an oversized bucket's split
-  long long tile, s, m;
+  unsigned long long cmin, cmax;  // (column, row) range of a tile
+  long long tile, s, m, col_base;
+  int wt;
 };
 
 template <class T>
@@ -412,17 +426,50 @@ __device__ long long bucket_chunk_reduce(BTileSmem<T>& S, long long b, int cm, l
 }
 
 // Sort a bucket held in S.sk / S.scol (tile positions, perm = identity) by
-// (column, row, input order): bins (column, high row bits) of ~4 keys,
-// counting pass, scan, scatter to S.u.sk2, then rank-in-bin placement back
-// into S.sk (long bins: warp / block bitonic).  Leaves S.scol in sorted order
-// and S.cstart[l] = first position of local column l (l = 0..W).
+// (column, row, input order).  Bins are aligned ranges of the composite
+// (column << row_bits | row) between the tile's min and max, at most kTBins
+// of them and never wider than one column; counting pass, scan, scatter to
+// S.u.sk2, then rank-in-bin placement back into S.sk (long bins: warp /
+// block bitonic).  Leaves S.scol in sorted order and S.cstart[l] = first
+// position of local column l (l = 0..Wt).  m >= 1.
 template <class T>
-__device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int W, int row_bits) {
+__device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int Wt, int row_bits) {
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
-  int lr = 0;
-  while (lr < row_bits && W * (2 << lr) <= kTBins && W * (2 << lr) * 4 <= m) lr++;
-  const int R = 1 << lr, sh = row_bits - lr, nbins = W * R;
-  auto bin_of = [&](int p) -> int { return (int)S.scol[p] * R + (int)(key_row(S.sk[p]) >> sh); };
+  auto comp = [&](int p) -> unsigned long long {
+    return ((unsigned long long)S.scol[p] << row_bits) | key_row(S.sk[p]);
+  };
+  if (tid == 0) {
+    S.cmin = ~0ull;
+    S.cmax = 0ull;
+  }
+  __syncthreads();
+  {
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int p = tid; p < m; p += nthr) {
+      const unsigned long long c = comp(p);
+      lo = min(lo, c);
+      hi = max(hi, c);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+      atomicMin(&S.cmin, lo);
+      atomicMax(&S.cmax, hi);
+    }
+  }
+  __syncthreads();
+  const unsigned long long cmin = S.cmin, cmax = S.cmax;
+  int sh = 0;
+  while (sh < row_bits && (cmax >> sh) - (cmin >> sh) + 1 > (unsigned long long)kTBins) sh++;
+  const unsigned long long cbase = cmin >> sh;
+  const int nbins = (int)((cmax >> sh) - cbase + 1);  // <= kTBins: at sh = row_bits it counts columns
+  auto bin_of = [&](int p) -> int { return (int)((comp(p) >> sh) - cbase); };
+  auto col_of_bin = [&](int b) -> unsigned short {
+    return (unsigned short)(((cbase + (unsigned long long)b) << sh) >> row_bits);
+  };
   for (int b = tid; b < nbins; b += nthr) S.v.bk.cursor[b] = 0u;
   __syncthreads();
   for (int p = tid; p < m; p += nthr) atomicAdd(&S.v.bk.cursor[bin_of(p)], 1u);
@@ -461,7 +508,10 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int W, int row_bits) {
     S.n_med = 0;
     S.n_big = 0;
   }
-  for (int l = tid; l <= W; l += nthr) S.cstart[l] = S.v.bk.bstart[l * R];
+  for (int l = tid; l <= Wt; l += nthr) {
+    const long long bl = (long long)(((unsigned long long)l << row_bits) >> sh) - (long long)cbase;
+    S.cstart[l] = S.v.bk.bstart[bl < 0 ? 0 : (bl > nbins ? nbins : bl)];
+  }
   __syncthreads();
   for (int b = tid; b < nbins; b += nthr) {
     const int L = S.v.bk.bstart[b + 1] - S.v.bk.bstart[b];
@@ -477,7 +527,7 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int W, int row_bits) {
       for (int j = s0; j < e0b; j++) r += (S.u.sk2[j] < k);
       S.sk[s0 + r] = k;
       S.perm[s0 + r] = S.perm2[q];
-      S.scol[s0 + r] = (unsigned short)(b / R);
+      S.scol[s0 + r] = col_of_bin(b);
     }
   }
   __syncthreads();
@@ -489,7 +539,7 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int W, int row_bits) {
     for (int i = lane; i < L; i += 32) {
       S.sk[s0 + i] = S.u.sk2[s0 + i];
       S.perm[s0 + i] = S.perm2[s0 + i];
-      S.scol[s0 + i] = (unsigned short)(b / R);
+      S.scol[s0 + i] = col_of_bin(b);
     }
   }
   for (int q = 0; q < n_big; q++) {
@@ -499,7 +549,7 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int W, int row_bits) {
     for (int i = tid; i < L; i += nthr) {
       S.sk[s0 + i] = S.u.sk2[s0 + i];
       S.perm[s0 + i] = S.perm2[s0 + i];
-      S.scol[s0 + i] = (unsigned short)(b / R);
+      S.scol[s0 + i] = col_of_bin(b);
     }
     __syncthreads();
   }
@@ -513,9 +563,9 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int W, int row_bits) {
 // global memory and streamed.  Values are read by input index.
 template <class T, class S1, class S2>
 __device__ void process_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a, long long s, long long m,
-                                         unsigned col_base, int wbits, int Wt) {
+                                         unsigned col_base, int Wt) {
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int W = 1 << wbits;
+  const int W = Wt;
   unsigned* bstart = S.obin;  // nbins + 1 u32 bin starts (bucket-relative)
   unsigned* cursor = reinterpret_cast<unsigned*>(&S.u) + kMaxW;  // [<= 2 * kTBins] (S.u is free here)
   unsigned long long* gk = a.keys + s;
@@ -610,8 +660,8 @@ __device__ void process_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1, S2>
       }
       run_base += ctot;
       __syncthreads();
-    } else if (L > kCap) {  // one bin above the tile: global radix sort, streamed reduce
-      int shifts[24], nbits[24], fromp[24], np = 0;
+    } else if (L > kCap) {  // one bin (one column) above the tile: global radix sort by (row, idx), streamed reduce
+      int shifts[16], nbits[16], fromp[16], np = 0;
       for (int bb = 0; bb < a.idx_bits; bb += 8) {
         shifts[np] = bb;
         nbits[np] = min(8, a.idx_bits - bb);
@@ -622,12 +672,6 @@ __device__ void process_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1, S2>
         shifts[np] = 32 + bb;
         nbits[np] = min(8, a.row_bits - bb);
         fromp[np] = 0;
-        np++;
-      }
-      for (int bb = 0; bb < wbits; bb += 8) {
-        shifts[np] = bb;
-        nbits[np] = min(8, wbits - bb);
-        fromp[np] = 1;
         np++;
       }
       __syncthreads();
@@ -680,7 +724,48 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
   if (a.pre_ptr != nullptr) {
     // pre-bucketed input (SpGEMM products): keys / colb / vals_b already sit
     // in output-column order; only the coarse bucket starts are needed
-    for (long long t = g * nthr + tid; t <= ncb; t += G * nthr) a.cb_start[t] = a.pre_ptr[min(t << wbits, a.n_cols)];
+    // variable-width buckets (kPreT): bucket t starts at the first column whose
+    // cumulative weight pre_ptr[c] + kPreColCost * c reaches t * kPreT;
+    // oversized buckets are queued first so the long ones start early
+    auto first_col = [&](long long target) -> long long {
+      long long lo = 0, hi = a.n_cols;
+      while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (__ldg(&a.pre_ptr[mid]) + kPreColCost * mid >= target) hi = mid;
+        else lo = mid + 1;
+      }
+      return lo;
+    };
+    for (long long t = g * nthr + tid; t < ncb; t += G * nthr) {
+      const long long c0 = first_col(t * kPreT);
+      const long long c1 = t + 1 == ncb ? a.n_cols : first_col((t + 1) * kPreT);
+      const long long s0 = __ldg(&a.pre_ptr[c0]);
+      a.cb_col[t] = (unsigned)c0;
+      a.cb_start[t] = s0;
+      if (t + 1 == ncb) {
+        a.cb_col[ncb] = (unsigned)a.n_cols;
+        a.cb_start[ncb] = __ldg(&a.pre_ptr[a.n_cols]);
+      }
+      // size class (largest first: a rough longest-processing-time order)
+      const long long mt = __ldg(&a.pre_ptr[c1]) - s0;
+      const unsigned cls = mt > 32 * kCap ? 0u : mt > 4 * kCap ? 1u : mt > kCap ? 2u : 3u;
+      const unsigned peers = __match_any_sync(__activemask(), cls);  // warp-aggregated slot
+      const int leader = __ffs(peers) - 1;
+      unsigned slot0 = 0;
+      if ((tid & 31) == leader) slot0 = atomicAdd(a.ticket + 1 + cls, (unsigned)__popc(peers));
+      slot0 = __shfl_sync(peers, slot0, leader);
+      a.cb_cnt[t] = (cls << 28) | (slot0 + __popc(peers & lanemask_lt()));
+    }
+    grid_sync(a.gb, gen);
+    {
+      unsigned base[4];
+      base[0] = 0;
+      for (int q = 1; q < 4; q++) base[q] = base[q - 1] + __ldcg(a.ticket + q);
+      for (long long t = g * nthr + tid; t < ncb; t += G * nthr) {
+        const unsigned v = __ldcg(&a.cb_cnt[t]);
+        a.order[base[v >> 28] + (v & 0x0fffffffu)] = (unsigned)t;
+      }
+    }
     grid_sync(a.gb, gen);
     AS_PHASE_MARK(a, gen);
   } else {
@@ -741,27 +826,37 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
   // ---------------- phase 4: bucket tiles ----------------
   while (true) {
     if (tid == 0) {
-      const long long t = (long long)atomicAdd(a.ticket, 1u);
+      long long t = (long long)atomicAdd(a.ticket, 1u);
+      if (t < ncb && a.order) t = __ldcg(&a.order[t]);
       S.tile = t;
       if (t < ncb) {
         S.s = __ldcg(&a.cb_start[t]);
         S.m = __ldcg(&a.cb_start[t + 1]) - S.s;
+        if (a.cb_col) {
+          S.col_base = __ldcg(&a.cb_col[t]);
+          S.wt = (int)(__ldcg(&a.cb_col[t + 1]) - S.col_base);
+        } else {
+          S.col_base = t << wbits;
+          S.wt = (int)min((long long)W, a.n_cols - S.col_base);
+        }
       }
     }
     __syncthreads();
     const long long t = S.tile;
     if (t >= ncb) break;
     const long long s = S.s, m = S.m;
-    const unsigned col_base = (unsigned)(t << wbits);
-    const int Wt = (int)min((long long)W, a.n_cols - (long long)col_base);  // columns of this bucket
-    if (m <= kCap) {
+    const unsigned col_base = (unsigned)S.col_base;
+    const int Wt = S.wt;  // columns of this bucket
+    if (m == 0) {
+      for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = 0u;
+    } else if (m <= kCap) {
       for (long long i = tid; i < m; i += nthr) {
         S.sk[i] = a.keys[s + i];
         S.scol[i] = (unsigned short)(a.colb[s + i] - col_base);
         S.perm[i] = (unsigned short)i;
       }
       __syncthreads();
-      sort_bucket_smem(S, (int)m, W, a.row_bits);
+      sort_bucket_smem(S, (int)m, Wt, a.row_bits);
       bucket_chunk_reduce<T>(S, 0, (int)m, m, nullptr, nullptr, col_base, a.vs, a.mode, a.prune, a.vals_b + s);
       for (int p = tid; p < m; p += nthr) {
         const unsigned e0 = S.v.excl[p], e1 = S.v.excl[p + 1];
@@ -772,7 +867,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
       }
       for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = S.v.excl[S.cstart[l + 1]] - S.v.excl[S.cstart[l]];
     } else {
-      process_oversized_bucket<T>(S, a, s, m, col_base, wbits, Wt);
+      process_oversized_bucket<T>(S, a, s, m, col_base, Wt);
     }
     __syncthreads();
   }
@@ -810,15 +905,79 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
   }
   grid_sync(a.gb, gen);
   AS_PHASE_MARK(a, gen);
-  for (long long t = g; t < ncb; t += G) {
-    const long long c0 = t << wbits;
-    const long long c1 = min(a.n_cols, c0 + W);
-    const long long dst = __ldcg(&a.col_ptr[c0]);
-    const long long cnt = __ldcg(&a.col_ptr[c1]) - dst;
-    const long long src = __ldcg(&a.cb_start[t]);
-    for (long long i = tid; i < cnt; i += nthr) {
-      a.row_idx[dst + i] = __ldcg(&a.tmp_rows[src + i]);
-      a.out_vals[dst + i] = __ldcg(&a.tmp_vals[src + i]);
+  {
+    // placement by equal output ranges (a heavy bucket is spread over many
+    // CTAs): bucket t's kept entries sit at tmp[cb_start[t] ...] and go to
+    // col_ptr[first column of t]; the bucket table of a range is staged in
+    // shared memory nthr buckets at a time
+    auto dst_of = [&](long long t) -> long long {
+      const long long c = t >= ncb ? a.n_cols
+                                   : (a.cb_col ? (long long)__ldcg(&a.cb_col[t]) : min(a.n_cols, t << wbits));
+      return __ldcg(&a.col_ptr[c]);
+    };
+    long long* sd = reinterpret_cast<long long*>(&S.u);  // [nthr + 1] bucket output starts
+    long long* ss = sd + (kSegThreads + 1);              // [nthr] bucket tmp starts
+    long long o0, o1;
+    cta_range(__ldcg(&a.col_ptr[a.n_cols]), g, G, &o0, &o1);
+    if (tid == 0) {
+      long long lo = 0, hi = ncb - 1;  // last t with dst(t) <= o0
+      while (lo < hi) {
+        const long long mid = (lo + hi + 1) >> 1;
+        if (dst_of(mid) <= o0) lo = mid;
+        else hi = mid - 1;
+      }
+      S.tile = lo;
+    }
+    __syncthreads();
+    long long tb = S.tile;
+    while (o0 < o1 && tb < ncb) {
+      const int nb = (int)min((long long)nthr, ncb - tb);
+      __syncthreads();
+      for (int i = tid; i <= nb; i += nthr) {
+        sd[i] = dst_of(tb + i);
+        if (i < nb) ss[i] = __ldcg(&a.cb_start[tb + i]);
+      }
+      __syncthreads();
+      const long long e = min(o1, sd[nb]);
+      int k = 0;  // bucket of this thread's next position: one search, then a forward walk
+      {
+        const long long o = o0 + tid;
+        int hi = nb - 1;
+        while (k < hi) {
+          const int mid = (k + hi + 1) >> 1;
+          if (sd[mid] <= o) k = mid;
+          else hi = mid - 1;
+        }
+      }
+      constexpr int kU = 4;
+      for (long long ob = o0 + tid; ob < e; ob += (long long)kU * nthr) {
+        long long src[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+          const long long o = ob + (long long)u * nthr;
+          src[u] = -1;
+          if (o < e) {
+            while (sd[k + 1] <= o) k++;
+            src[u] = ss[k] + (o - sd[k]);
+          }
+        }
+        int rr[kU];
+        T vv[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++)
+          if (src[u] >= 0) {
+            rr[u] = __ldcg(&a.tmp_rows[src[u]]);
+            vv[u] = __ldcg(&a.tmp_vals[src[u]]);
+          }
+#pragma unroll
+        for (int u = 0; u < kU; u++)
+          if (src[u] >= 0) {
+            a.row_idx[ob + (long long)u * nthr] = rr[u];
+            a.out_vals[ob + (long long)u * nthr] = vv[u];
+          }
+      }
+      o0 = max(o0, e);
+      tb += nb;
     }
   }
   __syncthreads();

@@ -27,6 +27,8 @@ struct PersistWs {
   unsigned* col_kept;
   long long* cta_sums;
   long long* own_info;
+  unsigned* cb_col;  // pre-bucketed input only
+  unsigned* order;
   int wbits;
   long long n_cb;
 };
@@ -42,14 +44,24 @@ static inline int choose_wbits(long long n, long long n_cols) {
   return ((n_cols + (1ll << wb) - 1) >> wb) > kMaxCoarse || (1 << wb) > kMaxW ? -1 : wb;
 }
 
-static size_t carve_persist(Carve& c, PersistWs* w, long long n, long long n_cols, size_t val_bytes) {
-  w->wbits = choose_wbits(n, n_cols);
-  const int wb = w->wbits < 0 ? 10 : w->wbits;
-  w->n_cb = (n_cols + (1ll << wb) - 1) >> wb;
+// pre = true: the input arrives bucketed by column (run_persist_ws pre_ptr);
+// buckets are then variable-width (kPreT), with no column-count limit.
+static size_t carve_persist(Carve& c, PersistWs* w, long long n, long long n_cols, size_t val_bytes,
+                            bool pre = false) {
+  if (pre) {
+    w->wbits = 0;
+    w->n_cb = (n + kPreColCost * n_cols) / kPreT + 1;
+  } else {
+    w->wbits = choose_wbits(n, n_cols);
+    const int wb = w->wbits < 0 ? 10 : w->wbits;
+    w->n_cb = (n_cols + (1ll << wb) - 1) >> wb;
+  }
   w->zero = c.take<unsigned>(64);
-  w->cb_cnt = c.take<unsigned>(std::max(1ll, w->n_cb));
+  w->cb_cnt = c.take<unsigned>(std::max(1ll, w->n_cb));  // pre: size class and slot of each bucket
   w->zero_bytes = c.off;
   w->cb_start = c.take<long long>(w->n_cb + 1);
+  w->cb_col = pre ? c.take<unsigned>(w->n_cb + 1) : nullptr;
+  w->order = pre ? c.take<unsigned>(w->n_cb) : nullptr;
   const long long n1 = std::max(1ll, n);
   w->keys = c.take<unsigned long long>(n1);
   w->keys_alt = c.take<unsigned long long>(n1);
@@ -126,6 +138,8 @@ static int run_persist_ws(PersistWs& w, const S1& s1, const S2& s2, long long n,
   a.gb = GridBar{w.zero + 16, w.zero + 32};
   a.phase_ts = nullptr;
   a.pre_ptr = pre_ptr;
+  a.cb_col = pre_ptr ? w.cb_col : nullptr;
+  a.order = pre_ptr ? w.order : nullptr;
   static unsigned long long* dbg_ts = nullptr;
   const bool phase_dbg = getenv("AS_PHASE_TIMES") != nullptr;
   if (phase_dbg) {
@@ -138,8 +152,12 @@ static int run_persist_ws(PersistWs& w, const S1& s1, const S2& s2, long long n,
     unsigned long long h[16];
     AS_CUDA_TRY(cudaMemcpyAsync(h, dbg_ts, sizeof(h), cudaMemcpyDeviceToHost, st));
     AS_CUDA_TRY(cudaStreamSynchronize(st));
-    fprintf(stderr, "[phases n=%lld n_cols=%lld W=%d n_cb=%lld]", n, n_cols, 1 << w.wbits, w.n_cb);
-    for (int i = 1; i < 16 && h[i]; i++) fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
+    fprintf(stderr, "[phases n=%lld n_cols=%lld W=%d n_cb=%lld]", n, n_cols, pre_ptr ? -1 : 1 << w.wbits, w.n_cb);
+    for (int i = 1, last = 0; i < 16; i++)
+      if (h[i]) {
+        fprintf(stderr, " %.2f", (h[i] - h[last]) * 1e-3);
+        last = i;
+      }
     fprintf(stderr, " us\n");
   }
   return rc;
@@ -158,10 +176,10 @@ static int run_persist(const S1& s1, const S2& s2, long long n_cols, int row_bit
                            init_info, nullptr, st);
 }
 
-inline size_t persist_ws_bytes(long long n, long long n_cols, size_t val_bytes) {
+inline size_t persist_ws_bytes(long long n, long long n_cols, size_t val_bytes, bool pre = false) {
   Carve c(nullptr, 0);
   PersistWs w;
-  carve_persist(c, &w, n, n_cols, val_bytes);
+  carve_persist(c, &w, n, n_cols, val_bytes, pre);
   return c.off;
 }
 

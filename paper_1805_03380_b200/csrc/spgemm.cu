@@ -9,15 +9,18 @@
 // B200 design (expand - sort - fold, bit-exact):
 //  1. as_spgemm_products: per column of B, the number of products
 //     (sum of |A[:,k]| over its entries) -> chained scan -> prod_ptr.
-//  2. expand: one warp per B column flattens its products in reference order
-//     (kk ascending, ii ascending) with a load-balanced warp scan, writing
-//     key = (row << 32) | product_index and the separately rounded product.
-//  3. the segmented tile engine (segsort.cuh) sorts each column's products by
-//     (row, product_index) -- the product index *is* the reference's
-//     accumulation order -- folds runs sequentially (kSumSeq), prunes zeros
-//     and compacts into CSC with one chained scan.  Columns whose products
-//     overflow shared memory are radix-sorted by row bits only, since they
-//     arrive already in index order.
+//  2. as_spgemm_f64 first scans the per-entry product counts of B
+//     (|A[:,b_rows[kk]]|) into ent_ptr, then expands with CTAs over equal
+//     ranges of products -- not over columns, so a 90k-product column costs
+//     what any 90k products cost.  Each CTA stages the B entries its range
+//     touches (start, A column start, b value, column) in shared memory and
+//     every thread locates its product with a shared-memory search; writes
+//     key = (row << 32) | product_index, the column and the separately
+//     rounded product, all coalesced.
+//  3. the persistent bucket kernel (persist.cuh, pre-bucketed mode) sorts
+//     each column's products by (row, product_index) -- the product index
+//     *is* the reference's accumulation order -- folds runs sequentially
+//     (kSumSeq), prunes zeros and compacts into CSC.
 #include "capi_util.cuh"
 #include "persist_host.cuh"
 
@@ -42,53 +45,125 @@ spgemm_count_kernel(long long n_cols_b, const int* __restrict__ a_ptr, const int
   }
 }
 
-// flatten the products of each B column in reference order
+// |A[:, b_rows[kk]]| for every entry of B
 __global__ void __launch_bounds__(kGThreads)
-spgemm_expand_kernel(long long n_cols_b, const int* __restrict__ a_ptr, const int* __restrict__ a_rows,
-                     const double* __restrict__ a_vals, const int* __restrict__ b_ptr, const int* __restrict__ b_rows,
-                     const double* __restrict__ b_vals, const long long* __restrict__ prod_ptr,
+spgemm_entry_len_kernel(long long nnz_b, const int* __restrict__ a_ptr, const int* __restrict__ b_rows,
+                        unsigned* __restrict__ lens) {
+  for (long long kk = (long long)blockIdx.x * blockDim.x + threadIdx.x; kk < nnz_b; kk += (long long)gridDim.x * blockDim.x) {
+    const int k = __ldg(&b_rows[kk]);
+    lens[kk] = (unsigned)(__ldg(&a_ptr[k + 1]) - __ldg(&a_ptr[k]));
+  }
+}
+
+constexpr int kExThreads = 256;
+constexpr int kExItems = 8;
+constexpr int kExRange = kExThreads * kExItems;  // products per CTA
+constexpr int kExWin = kExRange + 1;             // staged B entries (longer windows search globally)
+
+// Flatten products [t*kExRange, (t+1)*kExRange) in reference order (entry kk
+// ascending, A position ascending): product q belongs to the last entry with
+// ent_ptr[kk] <= q.
+__global__ void __launch_bounds__(kExThreads)
+spgemm_expand_kernel(long long nnz_b, long long n_cols_b, long long total, const int* __restrict__ a_ptr,
+                     const int* __restrict__ a_rows, const double* __restrict__ a_vals,
+                     const int* __restrict__ b_ptr, const int* __restrict__ b_rows,
+                     const double* __restrict__ b_vals, const long long* __restrict__ ent_ptr,
                      unsigned long long* __restrict__ keys, unsigned* __restrict__ colb, double* __restrict__ pvals) {
-  __shared__ int s_off[kGThreads / 32][33];
-  __shared__ int s_k[kGThreads / 32][32];
-  __shared__ double s_b[kGThreads / 32][32];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long j = (long long)blockIdx.x * (blockDim.x >> 5) + wib; j < n_cols_b; j += warps) {
-    long long out = prod_ptr[j];
-    const int kb = b_ptr[j], ke = b_ptr[j + 1];
-    for (int base = kb; base < ke; base += 32) {
-      const int kk = base + lane;
-      int len = 0, k = 0;
-      double bv = 0.0;
-      if (kk < ke) {
-        k = b_rows[kk];
-        bv = b_vals[kk];
-        len = a_ptr[k + 1] - a_ptr[k];
-      }
-      int inc = warp_inclusive_scan(len);
-      s_off[wib][lane + 1] = inc;
-      if (lane == 0) s_off[wib][0] = 0;
-      s_k[wib][lane] = a_ptr[k];
-      s_b[wib][lane] = bv;
-      const int total = __shfl_sync(0xffffffffu, inc, 31);
-      __syncwarp();
-      const int nent = min(32, ke - base);
-      for (int q = lane; q < total; q += 32) {
-        // entry e with s_off[e] <= q < s_off[e+1]
-        int lo = 0, hi = nent - 1;
+  __shared__ int s_off[kExWin];  // ent_ptr[kk] - P0 (clamped below at 0 for the first entry)
+  __shared__ int s_ast[kExWin];  // A column start of the entry, shifted to the entry's product 0
+  __shared__ int s_col[kExWin];
+  __shared__ double s_bv[kExWin];
+  __shared__ long long s_kk0, s_kk1, s_j0, s_j1;
+  const int tid = threadIdx.x;
+  for (long long t = blockIdx.x; t * kExRange < total; t += gridDim.x) {
+    const long long P0 = t * kExRange, P1 = min(total, P0 + kExRange);
+    __syncthreads();
+    if (tid == 0) {
+      // last entry with ent_ptr <= P0, and with ent_ptr <= P1 - 1
+      auto last_le = [&](long long q) {
+        long long lo = 0, hi = nnz_b - 1;
         while (lo < hi) {
-          int mid = (lo + hi + 1) >> 1;
-          if (s_off[wib][mid] <= q) lo = mid;
+          const long long mid = (lo + hi + 1) >> 1;
+          if (__ldg(&ent_ptr[mid]) <= q) lo = mid;
           else hi = mid - 1;
         }
-        const int ii = s_k[wib][lo] + (q - s_off[wib][lo]);
-        const long long pos = out + q;
-        keys[pos] = ((unsigned long long)(unsigned)a_rows[ii] << 32) | (unsigned long long)pos;
-        colb[pos] = (unsigned)j;
-        pvals[pos] = __dmul_rn(a_vals[ii], s_b[wib][lo]);
+        return lo;
+      };
+      const long long kk0 = last_le(P0), kk1 = last_le(P1 - 1);
+      auto col_of = [&](long long kk) {  // last j with b_ptr[j] <= kk
+        long long lo = 0, hi = n_cols_b - 1;
+        while (lo < hi) {
+          const long long mid = (lo + hi + 1) >> 1;
+          if (__ldg(&b_ptr[mid]) <= kk) lo = mid;
+          else hi = mid - 1;
+        }
+        return lo;
+      };
+      s_kk0 = kk0;
+      s_kk1 = kk1;
+      s_j0 = col_of(kk0);
+      s_j1 = col_of(kk1);
+    }
+    __syncthreads();
+    const long long kk0 = s_kk0, kk1 = s_kk1, j0 = s_j0, j1 = s_j1;
+    const int nw = (int)(kk1 - kk0 + 1);
+    const bool staged = nw <= kExWin;
+    if (staged) {
+      for (int e = tid; e < nw; e += kExThreads) {
+        const long long kk = kk0 + e;
+        const long long off = __ldg(&ent_ptr[kk]) - P0;
+        const int k = __ldg(&b_rows[kk]);
+        // entry kk's product p sits at A position a_ptr[k] + (q - ent_ptr[kk])
+        s_off[e] = (int)max(off, 0ll);
+        s_ast[e] = (int)(__ldg(&a_ptr[k]) - min(off, 0ll));
+        s_bv[e] = __ldg(&b_vals[kk]);
+        long long lo = j0, hi = j1;
+        while (lo < hi) {
+          const long long mid = (lo + hi + 1) >> 1;
+          if (__ldg(&b_ptr[mid]) <= kk) lo = mid;
+          else hi = mid - 1;
+        }
+        s_col[e] = (int)lo;
       }
-      out += total;
-      __syncwarp();
+      __syncthreads();
+    }
+    const int cnt = (int)(P1 - P0);
+#pragma unroll 2
+    for (int q = tid; q < cnt; q += kExThreads) {
+      int ii, col;
+      double bv;
+      if (staged) {
+        int lo = 0, hi = nw - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_off[mid] <= q) lo = mid;
+          else hi = mid - 1;
+        }
+        ii = s_ast[lo] + (q - s_off[lo]);
+        col = s_col[lo];
+        bv = s_bv[lo];
+      } else {  // many empty A columns in the window: search globally
+        long long lo = kk0, hi = kk1;
+        while (lo < hi) {
+          const long long mid = (lo + hi + 1) >> 1;
+          if (__ldg(&ent_ptr[mid]) <= P0 + q) lo = mid;
+          else hi = mid - 1;
+        }
+        const int k = __ldg(&b_rows[lo]);
+        ii = (int)(__ldg(&a_ptr[k]) + (P0 + q - __ldg(&ent_ptr[lo])));
+        bv = __ldg(&b_vals[lo]);
+        long long cl = j0, ch = j1;
+        while (cl < ch) {
+          const long long mid = (cl + ch + 1) >> 1;
+          if (__ldg(&b_ptr[mid]) <= lo) cl = mid;
+          else ch = mid - 1;
+        }
+        col = (int)cl;
+      }
+      const long long pos = P0 + q;
+      keys[pos] = ((unsigned long long)(unsigned)__ldg(&a_rows[ii]) << 32) | (unsigned long long)pos;
+      colb[pos] = (unsigned)col;
+      pvals[pos] = __dmul_rn(__ldg(&a_vals[ii]), bv);
     }
   }
 }
@@ -134,26 +209,60 @@ int as_spgemm_products(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, cons
   return AS_OK;
 }
 
-size_t as_spgemm_workspace_bytes(int64_t n_cols_b, int64_t total_products) {
-  return persist_ws_bytes(total_products, n_cols_b, sizeof(double));
+static void carve_spgemm(Carve& c, PersistWs* w, long long n_cols_b, long long nnz_b, long long total,
+                         unsigned** scan_zero, size_t* scan_zero_bytes, unsigned long long** states, unsigned** lens,
+                         long long** ent_ptr) {
+  carve_persist(c, w, total, n_cols_b, sizeof(double), true);
+  const long long per = (long long)kScanThreads * kScanItems;
+  const long long tiles = nnz_b > 0 ? (nnz_b + per - 1) / per : 1;
+  const size_t z0 = c.off;
+  *scan_zero = c.take<unsigned>(64);
+  *states = c.take<unsigned long long>(tiles);
+  *scan_zero_bytes = c.off - z0;
+  *lens = c.take<unsigned>(std::max(1ll, nnz_b));
+  *ent_ptr = c.take<long long>(nnz_b + 1);
+}
+
+size_t as_spgemm_workspace_bytes(int64_t n_cols_b, int64_t nnz_b, int64_t total_products) {
+  Carve c(nullptr, 0);
+  PersistWs w;
+  unsigned *z, *lens;
+  size_t zb;
+  unsigned long long* states;
+  long long* ent;
+  carve_spgemm(c, &w, n_cols_b, nnz_b, total_products, &z, &zb, &states, &lens, &ent);
+  return c.off;
 }
 
 int as_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int32_t* a_col_ptr,
                   const int32_t* a_row_idx, const double* a_vals, const int32_t* b_col_ptr, const int32_t* b_row_idx,
-                  const double* b_vals, const int64_t* prod_ptr, int64_t total_products, int32_t* col_ptr,
-                  int32_t* row_idx, double* out_vals, int64_t* info, void* ws, size_t ws_bytes, void* stream) {
+                  const double* b_vals, int64_t nnz_b, const int64_t* prod_ptr, int64_t total_products,
+                  int32_t* col_ptr, int32_t* row_idx, double* out_vals, int64_t* info, void* ws, size_t ws_bytes,
+                  void* stream) {
   cudaStream_t st = S(stream);
-  AS_REQUIRE(n_rows_a >= 0 && n_inner >= 0 && n_cols_b >= 0, AS_ERR_SHAPE, "negative dimension");
+  AS_REQUIRE(n_rows_a >= 0 && n_inner >= 0 && n_cols_b >= 0 && nnz_b >= 0, AS_ERR_SHAPE, "negative dimension");
   AS_REQUIRE(n_rows_a <= 0x7fffffffll && n_cols_b <= 0x7fffffffll, AS_ERR_SHAPE, "dimension outside int32 range");
   AS_REQUIRE(total_products >= 0 && total_products <= 0x7fffffffll, AS_ERR_ARG,
              "%lld products exceed the 31-bit product index", (long long)total_products);
   Carve c(ws, ws_bytes);
   PersistWs w;
-  carve_persist(c, &w, total_products, n_cols_b, sizeof(double));
+  unsigned *scan_zero, *lens;
+  size_t zb;
+  unsigned long long* states;
+  long long* ent_ptr;
+  carve_spgemm(c, &w, n_cols_b, nnz_b, total_products, &scan_zero, &zb, &states, &lens, &ent_ptr);
   AS_REQUIRE(c.ok, AS_ERR_ARG, "workspace too small: %zu < %zu", ws_bytes, c.off);
-  if (n_cols_b > 0 && total_products > 0) {
-    spgemm_expand_kernel<<<grid_for(n_cols_b * 32, kGThreads, 16), kGThreads, 0, st>>>(
-        n_cols_b, a_col_ptr, a_row_idx, a_vals, b_col_ptr, b_row_idx, b_vals, (const long long*)prod_ptr, w.keys,
+  if (n_cols_b > 0 && nnz_b > 0 && total_products > 0) {
+    const long long per = (long long)kScanThreads * kScanItems;
+    const long long tiles = (nnz_b + per - 1) / per;
+    AS_CUDA_TRY(cudaMemsetAsync(scan_zero, 0, zb, st));
+    spgemm_entry_len_kernel<<<grid_for(nnz_b, kGThreads), kGThreads, 0, st>>>(nnz_b, a_col_ptr, b_row_idx, lens);
+    AS_LAUNCH_CHECK();
+    count_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(lens, nnz_b, ent_ptr, states, scan_zero, nullptr, 0);
+    AS_LAUNCH_CHECK();
+    const long long ranges = (total_products + kExRange - 1) / kExRange;
+    spgemm_expand_kernel<<<(unsigned)std::min<long long>(ranges, (long long)kNumSMs * 32), kExThreads, 0, st>>>(
+        nnz_b, n_cols_b, total_products, a_col_ptr, a_row_idx, a_vals, b_col_ptr, b_row_idx, b_vals, ent_ptr, w.keys,
         w.colb, (double*)w.vals_b);
     AS_LAUNCH_CHECK();
   }

@@ -50,4 +50,4 @@ def test_version_and_workspace_sizes_host_only(lib):
     assert lib.as_build_workspace_bytes(1_000_000, 10_000) > 16 * 1_000_000
     assert lib.as_transpose_workspace_bytes(0, 0) > 0
     assert lib.as_trace_workspace_bytes(100, 10, 10) >= 256
-    assert lib.as_spgemm_workspace_bytes(5, 0) > 0
+    assert lib.as_spgemm_workspace_bytes(5, 0, 0) > 0
