@@ -179,7 +179,7 @@ def main_device(args):
     peak, peak_src = peaks()
     flush_buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
-    flush_scratch = torch.empty(1, dtype=torch.int64, device=dev)
+    flush_scratch = torch.empty((), dtype=torch.int64, device=dev)
 
     def l2_flush():
         # evict L2 by READING 512 MiB (a write-based flush leaves L2 full of

@@ -25,6 +25,36 @@ namespace as {
 
 constexpr int kMmThreads = 256;
 
+// L2 eviction-priority policy for the dense chunk: written by the transpose
+// and gathered ~nnz/n_cols times by the row kernel, it must outlive the
+// streams of A and C passing through L2 (evict_first / streaming hints).
+AS_DEVICE_INLINE unsigned long long l2_keep_policy() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+AS_DEVICE_INLINE void st_keep(float* p, float4 v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w), "l"(pol)
+               : "memory");
+}
+AS_DEVICE_INLINE void st_keep(double* p, double2 v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+               : "memory");
+}
+AS_DEVICE_INLINE float4 ld_keep(const float* p, unsigned long long pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+AS_DEVICE_INLINE double2 ld_keep(const double* p, unsigned long long pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+
 template <class T, int KC>
 __global__ void __launch_bounds__(kMmThreads)
 dense_chunk_transpose_kernel(long long n, const T* __restrict__ B, long long ldb, int kc, T* __restrict__ Bt) {
@@ -35,15 +65,11 @@ dense_chunk_transpose_kernel(long long n, const T* __restrict__ B, long long ldb
   for (int c = 0; c < KC; c++) v[c] = c < kc ? __ldcs(&B[j + (long long)c * ldb]) : T(0);
   T* dst = Bt + j * KC;
   constexpr int kVec = 16 / sizeof(T);
+  const unsigned long long pol = l2_keep_policy();
 #pragma unroll
   for (int c = 0; c < KC; c += kVec) {
-    if constexpr (sizeof(T) == 4) {
-      float4 q = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
-      *reinterpret_cast<float4*>(dst + c) = q;
-    } else {
-      double2 q = make_double2(v[c], v[c + 1]);
-      *reinterpret_cast<double2*>(dst + c) = q;
-    }
+    if constexpr (sizeof(T) == 4) st_keep(dst + c, make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]), pol);
+    else st_keep(dst + c, make_double2(v[c], v[c + 1]), pol);
   }
 }
 
@@ -122,6 +148,67 @@ spmm_rows_kernel(long long n_rows, const int* __restrict__ row_ptr, const int* _
     if (c < kc) __stcs(&C[r + (long long)c * ldc], (T)acc[c]);
 }
 
+// kL = 4 lanes per output row, each owning 16 bytes (4 f32 / 2 f64) of the
+// KC-wide chunk: one 128-bit gather per lane and entry, a whole 64-byte Bt
+// row per lane group; 8 rows per warp.  Few registers -> full occupancy and
+// many independent gathers in flight.  Entries are folded in CSR (column)
+// order, so exact mode keeps the reference's per-element order.
+template <class T, int KC, bool kExact>
+__global__ void __launch_bounds__(kMmThreads)
+spmm_rows_lanes_kernel(long long n_rows, const int* __restrict__ row_ptr, const int* __restrict__ col_idx,
+                       const T* __restrict__ vals, const T* __restrict__ Bt, int kc, T* __restrict__ C, long long ldc) {
+  constexpr int kVec = 16 / sizeof(T);
+  constexpr int kL = KC / kVec;
+  static_assert(32 % kL == 0, "lane groups must tile a warp");
+  using Acc = typename std::conditional<kExact, double, T>::type;
+  using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long r = gt / kL;
+  const int sub = (int)(gt % kL);
+  if (r >= n_rows) return;
+  const unsigned long long pol = l2_keep_policy();
+  Acc acc[kVec];
+#pragma unroll
+  for (int c = 0; c < kVec; c++) acc[c] = Acc(0);
+  const T* bt = Bt + sub * kVec;
+  auto fold = [&](T v, const V& b) {
+    const T* bb = reinterpret_cast<const T*>(&b);
+#pragma unroll
+    for (int c = 0; c < kVec; c++) {
+      if (kExact) {
+        if (bb[c] != T(0)) acc[c] = __dadd_rn(acc[c], __dmul_rn((double)v, (double)bb[c]));
+      } else {
+        acc[c] = fma_t(v, bb[c], acc[c]);
+      }
+    }
+  };
+  const int beg = __ldg(&row_ptr[r]), end = __ldg(&row_ptr[r + 1]);
+  // batches of kB entries: all indices, then all gathers (predicated), then
+  // the folds in entry order -- two dependent round trips per batch
+  constexpr int kB = 8;
+  for (int k = beg; k < end; k += kB) {
+    int j[kB];
+    T v[kB];
+#pragma unroll
+    for (int u = 0; u < kB; u++) {
+      j[u] = k + u < end ? __ldcs(&col_idx[k + u]) : -1;
+      v[u] = k + u < end ? __ldcs(&vals[k + u]) : T(0);
+    }
+    V b[kB];
+#pragma unroll
+    for (int u = 0; u < kB; u++)
+      if (j[u] >= 0) b[u] = ld_keep(bt + (long long)j[u] * KC, pol);
+#pragma unroll
+    for (int u = 0; u < kB; u++)
+      if (j[u] >= 0) fold(v[u], b[u]);
+  }
+#pragma unroll
+  for (int c = 0; c < kVec; c++) {
+    const int col = sub * kVec + c;
+    if (col < kc) __stcs(&C[r + (long long)col * ldc], (T)acc[c]);
+  }
+}
+
 // k == 1 exact: y = A x as a per-row left fold (mat_times_vec, bit-exact)
 template <class T>
 __global__ void __launch_bounds__(kMmThreads)
@@ -154,7 +241,8 @@ vecmat_csc_kernel(long long n_cols, const int* __restrict__ col_ptr, const int* 
 template <class T, int KC, bool kExact>
 static int spmm_impl(long long n_rows, long long n_cols, long long k, const int* row_ptr, const int* col_idx,
                      const T* vals, const T* B, long long ldb, T* C, long long ldc, T* Bt, cudaStream_t st) {
-  const int blocks_r = (int)((n_rows + kMmThreads - 1) / kMmThreads);
+  constexpr int kL = KC / (16 / sizeof(T));
+  const long long blocks_r = (n_rows * kL + kMmThreads - 1) / kMmThreads;
   const int blocks_c = (int)((n_cols + kMmThreads - 1) / kMmThreads);
   for (long long k0 = 0; k0 < k; k0 += KC) {
     const int kc = (int)min((long long)KC, k - k0);
@@ -163,8 +251,8 @@ static int spmm_impl(long long n_rows, long long n_cols, long long k, const int*
       AS_LAUNCH_CHECK();
     }
     if (n_rows > 0) {
-      spmm_rows_kernel<T, KC, kExact><<<blocks_r, kMmThreads, 0, st>>>(n_rows, row_ptr, col_idx, vals, Bt, kc,
-                                                                       C + k0 * ldc, ldc);
+      spmm_rows_lanes_kernel<T, KC, kExact><<<(unsigned)blocks_r, kMmThreads, 0, st>>>(n_rows, row_ptr, col_idx,
+                                                                                      vals, Bt, kc, C + k0 * ldc, ldc);
       AS_LAUNCH_CHECK();
     }
   }
