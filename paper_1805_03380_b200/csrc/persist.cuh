@@ -46,13 +46,14 @@ constexpr int kVisitVec = 4;  // consecutive elements per thread (ILP)
 
 template <class IdxT>
 AS_DEVICE_INLINE void load_vec4(const IdxT* p, long long i, long long hi, long long* out) {
-  if (i + 3 < hi && sizeof(IdxT) == 4 && ((i & 3) == 0)) {
+  const bool al = ((reinterpret_cast<unsigned long long>(p + i) & 15ull) == 0);  // any base pointer
+  if (i + 3 < hi && sizeof(IdxT) == 4 && al) {
     const int4 q = __ldg(reinterpret_cast<const int4*>(p + i));
     out[0] = q.x;
     out[1] = q.y;
     out[2] = q.z;
     out[3] = q.w;
-  } else if (i + 3 < hi && sizeof(IdxT) == 8 && ((i & 1) == 0)) {
+  } else if (i + 3 < hi && sizeof(IdxT) == 8 && al) {
     const longlong2 a = __ldg(reinterpret_cast<const longlong2*>(p + i));
     const longlong2 b = __ldg(reinterpret_cast<const longlong2*>(p + i + 2));
     out[0] = a.x;
@@ -62,6 +63,29 @@ AS_DEVICE_INLINE void load_vec4(const IdxT* p, long long i, long long hi, long l
   } else {
 #pragma unroll
     for (int k = 0; k < 4; k++) out[k] = (i + k < hi) ? (long long)__ldg(&p[i + k]) : 0;
+  }
+}
+
+// four consecutive values (128-bit loads when aligned)
+template <class T>
+AS_DEVICE_INLINE void load_vals4(const T* p, long long i, long long hi, T* out) {
+  const bool al = ((reinterpret_cast<unsigned long long>(p + i) & 15ull) == 0);
+  if (i + 3 < hi && sizeof(T) == 8 && al) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p + i));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p + i + 2));
+    out[0] = (T)a.x;
+    out[1] = (T)a.y;
+    out[2] = (T)b.x;
+    out[3] = (T)b.y;
+  } else if (i + 3 < hi && sizeof(T) == 4 && al) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p + i));
+    out[0] = (T)a.x;
+    out[1] = (T)a.y;
+    out[2] = (T)a.z;
+    out[3] = (T)a.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; k++) out[k] = (i + k < hi) ? __ldg(&p[i + k]) : T(0);
   }
 }
 
@@ -75,14 +99,18 @@ struct CooSrc {
   unsigned long long idx_off;
   long long* bad;  // first invalid triplet (reported in phase 1)
 
-  template <class F>
+  // f(col, minor, idx, i, value); kVal: the values are loaded with the
+  // indices (vectorised) so the scatter does not wait on a late scalar load
+  template <bool kVal = false, class F>
   __device__ void visit(long long p, long long P, bool report, F f) const {
     const long long ch = (((n + P - 1) / P) + 3) & ~3ll;
     const long long lo = min(n, p * ch), hi = min(n, lo + ch);
     for (long long i = lo + (long long)threadIdx.x * kVisitVec; i < hi; i += (long long)blockDim.x * kVisitVec) {
       long long r[4], c[4];
+      T v[4] = {T(0), T(0), T(0), T(0)};
       load_vec4(rows, i, hi, r);
       load_vec4(cols, i, hi, c);
+      if (kVal) load_vals4(vals, i, hi, v);
 #pragma unroll
       for (int k = 0; k < 4; k++) {
         const long long e = i + k;
@@ -91,7 +119,7 @@ struct CooSrc {
           if (report && bad) atomicMin((unsigned long long*)bad, (unsigned long long)e);
           continue;
         }
-        f((unsigned)c[k], (unsigned)r[k], (unsigned long long)e + idx_off, e);
+        f((unsigned)c[k], (unsigned)r[k], (unsigned long long)e + idx_off, e, v[k]);
       }
     }
   }
@@ -117,7 +145,7 @@ struct CscSrc {
   unsigned long long idx_off;
   int* colc;
 
-  template <class F>
+  template <bool kVal = false, class F>
   __device__ void visit(long long p, long long P, bool report, F f) const {
     (void)report;
     __shared__ long long s_cb, s_ce;
@@ -150,14 +178,16 @@ struct CscSrc {
         c = upper_bound_dev(col_ptr + cb, ce - cb + 1, (int)i) - 1 + cb;
       }
       long long r[4];
+      T v[4] = {T(0), T(0), T(0), T(0)};
       load_vec4(row_idx, i, hi, r);
+      if (kVal) load_vals4(vals, i, hi, v);
 #pragma unroll
       for (int k = 0; k < 4; k++) {
         const long long e = i + k;
         if (e >= hi) break;
         while ((cached ? colc[c + 1 - cb] : col_ptr[c + 1]) <= e) c++;
-        if (by_row) f((unsigned)r[k], (unsigned)c, (unsigned long long)e + idx_off, e);
-        else f((unsigned)c, (unsigned)r[k], (unsigned long long)e + idx_off, e);
+        if (by_row) f((unsigned)r[k], (unsigned)c, (unsigned long long)e + idx_off, e, v[k]);
+        else f((unsigned)c, (unsigned)r[k], (unsigned long long)e + idx_off, e, v[k]);
       }
     }
     __syncthreads();
@@ -169,7 +199,7 @@ struct CscSrc {
 
 template <class T>
 struct NoSrc {
-  template <class F>
+  template <bool kVal = false, class F>
   __device__ void visit(long long, long long, bool, F) const {}
   AS_DEVICE_INLINE T value(long long) const { return T(0); }
   __host__ __device__ long long size() const { return 0; }
@@ -773,7 +803,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
   for (long long b = tid; b < ncb; b += nthr) SM.h.a[b] = 0u;
   __syncthreads();
   {
-    auto inc = [&](unsigned c, unsigned, unsigned long long, long long) { atomicAdd(&SM.h.a[c >> wbits], 1u); };
+    auto inc = [&](unsigned c, unsigned, unsigned long long, long long, T) { atomicAdd(&SM.h.a[c >> wbits], 1u); };
     a.s1.visit(g, G, true, inc);
     a.s2.visit(g, G, true, inc);
   }
@@ -805,19 +835,19 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
   __syncthreads();
 
   // ---------------- phase 3: scatter keys, columns and values ----------------
-  a.s1.visit(g, G, false, [&](unsigned c, unsigned minor, unsigned long long idx, long long i) {
+  a.s1.template visit<true>(g, G, false, [&](unsigned c, unsigned minor, unsigned long long idx, long long, T v) {
     const unsigned cb = c >> wbits;
     const unsigned slot = SM.h.b[cb] + atomicAdd(&SM.h.a[cb], 1u);
     a.keys[slot] = ((unsigned long long)minor << 32) | idx;
     a.colb[slot] = c;
-    a.vals_b[slot] = a.s1.value(i);
+    a.vals_b[slot] = v;
   });
-  a.s2.visit(g, G, false, [&](unsigned c, unsigned minor, unsigned long long idx, long long i) {
+  a.s2.template visit<true>(g, G, false, [&](unsigned c, unsigned minor, unsigned long long idx, long long, T v) {
     const unsigned cb = c >> wbits;
     const unsigned slot = SM.h.b[cb] + atomicAdd(&SM.h.a[cb], 1u);
     a.keys[slot] = ((unsigned long long)minor << 32) | idx;
     a.colb[slot] = c;
-    a.vals_b[slot] = a.s2.value(i);
+    a.vals_b[slot] = v;
   });
   grid_sync(a.gb, gen);
   AS_PHASE_MARK(a, gen);

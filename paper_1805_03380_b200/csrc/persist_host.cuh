@@ -37,9 +37,10 @@ struct PersistWs {
 // bucket on average, at most kMaxCoarse buckets.  Returns -1 when the column
 // count exceeds kMaxCoarse * kMaxW.
 static inline int choose_wbits(long long n, long long n_cols) {
+  static const double kFill = getenv("AS_FILL") ? atof(getenv("AS_FILL")) : 0.8;
   const double avg = n_cols > 0 ? (double)n / (double)n_cols : 0.0;
   int wb = 0;
-  while ((1 << (wb + 1)) <= kMaxW && (double)(1 << (wb + 1)) * avg <= 0.8 * kCap) wb++;
+  while ((1 << (wb + 1)) <= kMaxW && (double)(1 << (wb + 1)) * avg <= kFill * kCap) wb++;
   while (wb <= 10 && ((n_cols + (1ll << wb) - 1) >> wb) > kMaxCoarse) wb++;
   return ((n_cols + (1ll << wb) - 1) >> wb) > kMaxCoarse || (1 << wb) > kMaxW ? -1 : wb;
 }
