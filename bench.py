@@ -319,16 +319,38 @@ def main_device(args):
                        "index_dtype": "int32 device", "l2": "flushed before every step (512 MiB device read, %s)" % args.flush,
                        "parallelism": "independent batch per GPU" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": build_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": build_gbs / peak, "traffic": None, "peak_source": peak_src,
-                         "kernel": "as_coo_to_csc_f64 (count, scan, scatter, seg_tile: 4 kernels)",
+                         "frac": build_gbs / peak, "traffic": ncu_traffic("build"), "peak_source": peak_src,
+                         "traffic_source": TRAFFIC_SRC,
+                         "kernel": "as_coo_to_csc_f64 (one persistent cooperative kernel + 2 memsets)",
                          "algorithmic_bytes": build_bytes},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 4 * args.steps, "clocks": clocks, "ops": ops,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 1 * args.steps, "clocks": clocks, "ops": ops,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def _load_traffic():
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of
+    each op's dominant kernel from the newest committed `ncu --set full`
+    capture (profiles/rNN_traffic.json, made by tools/ncu_traffic.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*_traffic.json")))
+    if not files:
+        return {}, None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    return d, "ncu --set full, " + os.path.basename(files[-1])
+
+
+_TRAFFIC, TRAFFIC_SRC = _load_traffic()
+
+
+def ncu_traffic(op):
+    k = _TRAFFIC.get(op)
+    return None if k is None else k["dram_read"] + k["dram_write"]
 
 
 def bench_ops(args, dev, L, sp, timed, peak):
@@ -358,7 +380,8 @@ def bench_ops(args, dev, L, sp, timed, peak):
         gbs = alg_bytes / (ms * 1e-3) / 1e9
         d = {"ms": ms, "value": units / (ms * 1e-3), "unit": unit,
              "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-                          "algorithmic_bytes": alg_bytes}, "parity": parity}
+                          "algorithmic_bytes": alg_bytes, "traffic": ncu_traffic(name.split("_")[0])},
+             "parity": parity}
         if extra:
             d.update(extra)
         out[name] = d
@@ -385,7 +408,7 @@ def bench_ops(args, dev, L, sp, timed, peak):
         if not same_csc((tp, tr, tv), oracle.transpose(n_rows, n_cols, *a)):
             raise CorrectnessError("transpose differs from the oracle")
         record("transpose_cfg1", timed(f, K, W), nnz, "nnz/s",
-               24 * nnz + 4 * (n_cols + 1) + 4 * (n_rows + 1), "bit-exact", {"launches": 4})
+               24 * nnz + 4 * (n_cols + 1) + 4 * (n_rows + 1), "bit-exact", {"launches": 1})
 
     # insertion-log flush (cfg2)
     if "flush" in want_ops:
@@ -412,7 +435,7 @@ def bench_ops(args, dev, L, sp, timed, peak):
         if not same_csc((op_, orr[:nnz], ov[:nnz]), want):
             raise CorrectnessError("flush differs from the oracle")
         record("flush_cfg2", timed(f, K, W), nl, "writes/s", 12 * nl + 12 * nnz + 4 * (n_c + 1), "bit-exact",
-               {"nnz_out": nnz, "launches": 4})
+               {"nnz_out": nnz, "launches": 1})
 
     # SpMM (cfg3)
     if "spmm" in want_ops:

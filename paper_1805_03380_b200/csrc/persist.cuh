@@ -17,19 +17,25 @@
 //   3 scatter           each chunk re-read; slot = bucket start + CTA range +
 //                       shared cursor; key (row << 32 | input index), column
 //                       and value moved to the slot.            [grid barrier]
-//   4 bucket tiles      a CTA per bucket sorts it by (column, row, input
-//                       order) in shared memory -- bins (column, high row
-//                       bits) of ~4 keys, every key ranking itself in its bin
-//                       -- reduces runs in the reference order, prunes zeros,
-//                       writes the compacted bucket to temporaries and the
-//                       kept count of each column.  Buckets larger than the
-//                       tile are radix-sorted in global memory and streamed.
+//   4 bucket tiles      a CTA per bucket (dynamic tickets) sorts it by
+//                       (column, row, input order) in shared memory -- up to
+//                       1024 bins over the tile's (column, row) range, every
+//                       key ranking itself in its bin -- reduces runs in the
+//                       reference order, prunes zeros, writes the compacted
+//                       bucket to temporaries and the kept count of each
+//                       column.  Buckets larger than the tile are split in
+//                       global memory into per-column row-prefix bins and
+//                       processed a tile-sized group of bins at a time.
 //                                                               [grid barrier]
-//   5 columns           grid-wide scan of the kept counts -> col_ptr; each
-//                       bucket copied to its final offset.      [2 barriers]
+//   5 columns           grid-wide scan of the kept counts -> col_ptr; output
+//                       ranges copied to their final offsets.   [2 barriers]
+//
+// Pre-bucketed mode (pre_ptr != nullptr, SpGEMM): the input already sits in
+// column order, phases 1-3 are replaced by variable-width buckets computed
+// from pre_ptr (kPreT) and queued largest size class first.
 #pragma once
 
-#include "segsort.cuh"
+#include "tile_common.cuh"
 
 namespace as {
 

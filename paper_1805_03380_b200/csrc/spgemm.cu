@@ -202,8 +202,7 @@ int as_spgemm_products(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, cons
                                                                                    b_row_idx, counts);
     AS_LAUNCH_CHECK();
   }
-  count_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(counts, n_cols_b, (long long*)prod_ptr, states, ticket,
-                                                              nullptr, 0);
+  count_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(counts, n_cols_b, (long long*)prod_ptr, states, ticket);
   AS_LAUNCH_CHECK();
   AS_CUDA_TRY(cudaMemcpyAsync(info, prod_ptr + n_cols_b, sizeof(long long), cudaMemcpyDeviceToDevice, st));
   return AS_OK;
@@ -258,7 +257,7 @@ int as_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int
     AS_CUDA_TRY(cudaMemsetAsync(scan_zero, 0, zb, st));
     spgemm_entry_len_kernel<<<grid_for(nnz_b, kGThreads), kGThreads, 0, st>>>(nnz_b, a_col_ptr, b_row_idx, lens);
     AS_LAUNCH_CHECK();
-    count_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(lens, nnz_b, ent_ptr, states, scan_zero, nullptr, 0);
+    count_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(lens, nnz_b, ent_ptr, states, scan_zero);
     AS_LAUNCH_CHECK();
     const long long ranges = (total_products + kExRange - 1) / kExRange;
     spgemm_expand_kernel<<<(unsigned)std::min<long long>(ranges, (long long)kNumSMs * 32), kExThreads, 0, st>>>(
