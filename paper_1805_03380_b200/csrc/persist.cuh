@@ -223,7 +223,7 @@ struct PersistArgs {
   S2 s2;
   long long n_cols;   // output columns (fine buckets)
   long long n_upper;  // s1.size() + s2.size()
-  int wbits;          // coarse bucket = column >> wbits
+  unsigned long long cb_mul;  // coarse bucket = (column * cb_mul) >> 32 (phases 1-3)
   long long n_cb;
   unsigned* cb_cnt;       // [n_cb] zeroed
   long long* cb_start;    // [n_cb + 1]
@@ -247,10 +247,10 @@ struct PersistArgs {
   GridBar gb;
   unsigned long long* phase_ts;  // optional: globaltimer after each phase (debug)
   const long long* pre_ptr;      // non-null: input already bucketed by column (SpGEMM products)
-  // pre_ptr only: variable-width buckets -- bucket t spans columns
-  // [cb_col[t], cb_col[t+1]); tiles are taken in `order` (oversized first)
+  // bucket t spans columns [cb_col[t], cb_col[t+1]); pre_ptr mode: tiles are
+  // taken in `order` (largest size class first)
   unsigned* cb_col;              // [n_cb + 1]
-  unsigned* order;               // [n_cb]
+  unsigned* order;               // [n_cb] (pre_ptr mode only)
 };
 
 // Variable-width buckets of pre-bucketed input: column c weighs
@@ -401,7 +401,18 @@ __device__ long long bucket_chunk_reduce(BTileSmem<T>& S, long long b, int cm, l
                                          const unsigned long long* gk, const unsigned* gcol, unsigned col_base,
                                          VS vs, int mode, int prune, const T* vslot) {
   const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  for (int base = 0; base < cm; base += nthr) {
+  // all value gathers of this thread issued before any is used (L2 latency
+  // once per tile, not once per position)
+  T vv[kItems];
+#pragma unroll
+  for (int q = 0; q < kItems; q++) {
+    const int p = q * kSegThreads + tid;
+    if (p < cm) vv[q] = vslot ? vslot[S.perm[p]] : vs((unsigned long long)key_idx(S.sk[p]));
+  }
+#pragma unroll
+  for (int q = 0; q < kItems; q++) {
+    const int base = q * kSegThreads;
+    if (base >= cm) break;
     const int p = base + tid;
     bool head = false;
     if (p < cm) {
@@ -409,10 +420,15 @@ __device__ long long bucket_chunk_reduce(BTileSmem<T>& S, long long b, int cm, l
       const unsigned row = key_row(k), col = S.scol[p];
       if (p > 0) head = row != key_row(S.sk[p - 1]) || col != S.scol[p - 1];
       else head = (b == 0) || row != key_row(gk[b - 1]) || col != gcol[b - 1] - col_base;
-      S.u.rv[p] = vslot ? vslot[S.perm[p]] : vs((unsigned long long)key_idx(k));
     }
     const unsigned hb = __ballot_sync(0xffffffffu, head);
     if (lane == 0 && base + warp * 32 < cm) S.hbits[(base >> 5) + warp] = hb;
+  }
+  __syncthreads();  // every read of S.u (as sk2) is done before rv overwrites it
+#pragma unroll
+  for (int q = 0; q < kItems; q++) {
+    const int p = q * kSegThreads + tid;
+    if (p < cm) S.u.rv[p] = vv[q];
   }
   __syncthreads();
   const int pb = tid * kItems, pe = min(pb + kItems, cm);
@@ -752,7 +768,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
   const int tid = threadIdx.x, nthr = blockDim.x;
   const long long G = gridDim.x, g = blockIdx.x;
   const long long ncb = a.n_cb;
-  const int wbits = a.wbits, W = 1 << wbits;
+  const unsigned long long cb_mul = a.cb_mul;
+  auto bucket_of = [&](unsigned c) -> unsigned { return (unsigned)(((unsigned long long)c * cb_mul) >> 32); };
   AS_PHASE_MARK(a, 0);
   a.s1.set_cache(SM.h.colc);
   a.s2.set_cache(SM.h.colc);
@@ -806,10 +823,16 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
     AS_PHASE_MARK(a, gen);
   } else {
   // ---------------- phase 1: coarse histogram + range reservation ----------------
+  // bucket(c) = (c * cb_mul) >> 32: monotone, ~n_cols / n_cb columns each;
+  // bucket t starts at the first column with bucket(c) >= t
+  for (long long t = g * nthr + tid; t <= ncb; t += G * nthr) {
+    const unsigned long long c0 = cb_mul ? (((unsigned long long)t << 32) + cb_mul - 1) / cb_mul : 0ull;
+    a.cb_col[t] = (unsigned)(t == ncb ? a.n_cols : min((long long)c0, a.n_cols));
+  }
   for (long long b = tid; b < ncb; b += nthr) SM.h.a[b] = 0u;
   __syncthreads();
   {
-    auto inc = [&](unsigned c, unsigned, unsigned long long, long long, T) { atomicAdd(&SM.h.a[c >> wbits], 1u); };
+    auto inc = [&](unsigned c, unsigned, unsigned long long, long long, T) { atomicAdd(&SM.h.a[bucket_of(c)], 1u); };
     a.s1.visit(g, G, true, inc);
     a.s2.visit(g, G, true, inc);
   }
@@ -842,14 +865,14 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
 
   // ---------------- phase 3: scatter keys, columns and values ----------------
   a.s1.template visit<true>(g, G, false, [&](unsigned c, unsigned minor, unsigned long long idx, long long, T v) {
-    const unsigned cb = c >> wbits;
+    const unsigned cb = bucket_of(c);
     const unsigned slot = SM.h.b[cb] + atomicAdd(&SM.h.a[cb], 1u);
     a.keys[slot] = ((unsigned long long)minor << 32) | idx;
     a.colb[slot] = c;
     a.vals_b[slot] = v;
   });
   a.s2.template visit<true>(g, G, false, [&](unsigned c, unsigned minor, unsigned long long idx, long long, T v) {
-    const unsigned cb = c >> wbits;
+    const unsigned cb = bucket_of(c);
     const unsigned slot = SM.h.b[cb] + atomicAdd(&SM.h.a[cb], 1u);
     a.keys[slot] = ((unsigned long long)minor << 32) | idx;
     a.colb[slot] = c;
@@ -868,13 +891,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
       if (t < ncb) {
         S.s = __ldcg(&a.cb_start[t]);
         S.m = __ldcg(&a.cb_start[t + 1]) - S.s;
-        if (a.cb_col) {
-          S.col_base = __ldcg(&a.cb_col[t]);
-          S.wt = (int)(__ldcg(&a.cb_col[t + 1]) - S.col_base);
-        } else {
-          S.col_base = t << wbits;
-          S.wt = (int)min((long long)W, a.n_cols - S.col_base);
-        }
+        S.col_base = __ldcg(&a.cb_col[t]);
+        S.wt = (int)(__ldcg(&a.cb_col[t + 1]) - S.col_base);
       }
     }
     __syncthreads();
@@ -886,14 +904,45 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
     if (m == 0) {
       for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = 0u;
     } else if (m <= kCap) {
-      for (long long i = tid; i < m; i += nthr) {
-        S.sk[i] = a.keys[s + i];
-        S.scol[i] = (unsigned short)(a.colb[s + i] - col_base);
-        S.perm[i] = (unsigned short)i;
+      long long t_last = a.phase_ts ? clock64() : 0;
+      // debug (AS_PHASE_TIMES): cycles of each tile step summed over all tiles
+      auto tile_mark = [&](int k) {
+        if (a.phase_ts) {
+          __syncthreads();
+          if (tid == 0) {
+            const long long now = clock64();
+            atomicAdd(&a.phase_ts[8 + k], (unsigned long long)(now - t_last));
+            t_last = now;
+          }
+        }
+      };
+      {
+        unsigned long long kk[kItems];
+        unsigned cc[kItems];
+#pragma unroll
+        for (int q = 0; q < kItems; q++) {
+          const int i = q * kSegThreads + tid;
+          if (i < m) {
+            kk[q] = __ldcg(&a.keys[s + i]);
+            cc[q] = __ldcg(&a.colb[s + i]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kItems; q++) {
+          const int i = q * kSegThreads + tid;
+          if (i < m) {
+            S.sk[i] = kk[q];
+            S.scol[i] = (unsigned short)(cc[q] - col_base);
+            S.perm[i] = (unsigned short)i;
+          }
+        }
       }
       __syncthreads();
+      tile_mark(0);
       sort_bucket_smem(S, (int)m, Wt, a.row_bits);
+      tile_mark(1);
       bucket_chunk_reduce<T>(S, 0, (int)m, m, nullptr, nullptr, col_base, a.vs, a.mode, a.prune, a.vals_b + s);
+      tile_mark(2);
       for (int p = tid; p < m; p += nthr) {
         const unsigned e0 = S.v.excl[p], e1 = S.v.excl[p + 1];
         if (e1 != e0) {
@@ -902,6 +951,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
         }
       }
       for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = S.v.excl[S.cstart[l + 1]] - S.v.excl[S.cstart[l]];
+      tile_mark(3);
     } else {
       process_oversized_bucket<T>(S, a, s, m, col_base, Wt);
     }
@@ -947,8 +997,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
     // col_ptr[first column of t]; the bucket table of a range is staged in
     // shared memory nthr buckets at a time
     auto dst_of = [&](long long t) -> long long {
-      const long long c = t >= ncb ? a.n_cols
-                                   : (a.cb_col ? (long long)__ldcg(&a.cb_col[t]) : min(a.n_cols, t << wbits));
+      const long long c = t >= ncb ? a.n_cols : (long long)__ldcg(&a.cb_col[t]);
       return __ldcg(&a.col_ptr[c]);
     };
     long long* sd = reinterpret_cast<long long*>(&S.u);  // [nthr + 1] bucket output starts

@@ -27,41 +27,54 @@ struct PersistWs {
   unsigned* col_kept;
   long long* cta_sums;
   long long* own_info;
-  unsigned* cb_col;  // pre-bucketed input only
-  unsigned* order;
-  int wbits;
+  unsigned* cb_col;  // [n_cb + 1] first column of each bucket
+  unsigned* order;   // pre-bucketed input only
+  unsigned long long cb_mul;
+  bool ok;           // the column count is supported
   long long n_cb;
 };
 
-// Coarse buckets of W = 2^wbits output columns: ~0.8 * kCap elements per
-// bucket on average, at most kMaxCoarse buckets.  Returns -1 when the column
-// count exceeds kMaxCoarse * kMaxW.
-static inline int choose_wbits(long long n, long long n_cols) {
+// Coarse buckets of ~n_cols / n_cb consecutive output columns (bucket(c) =
+// (c * cb_mul) >> 32).  n_cb: ~0.8 * kCap elements per bucket on average,
+// rounded up to whole waves of the co-resident grid (kNumSMs x 3 CTAs) when
+// above one wave, so the tile phase has no half-empty last wave; at least n_cols / kMaxBucketCols
+// (a bucket's columns index shared arrays), at most kMaxCoarse.  Returns 0
+// when the column count exceeds kMaxCoarse * kMaxBucketCols.
+constexpr long long kMaxBucketCols = kMaxW - 24;
+
+static inline long long choose_ncb(long long n, long long n_cols) {
   static const double kFill = getenv("AS_FILL") ? atof(getenv("AS_FILL")) : 0.8;
-  const double avg = n_cols > 0 ? (double)n / (double)n_cols : 0.0;
-  int wb = 0;
-  while ((1 << (wb + 1)) <= kMaxW && (double)(1 << (wb + 1)) * avg <= kFill * kCap) wb++;
-  while (wb <= 10 && ((n_cols + (1ll << wb) - 1) >> wb) > kMaxCoarse) wb++;
-  return ((n_cols + (1ll << wb) - 1) >> wb) > kMaxCoarse || (1 << wb) > kMaxW ? -1 : wb;
+  const long long wave = (long long)kNumSMs * 3;
+  long long nb = (long long)((double)n / (kFill * kCap)) + 1;
+  static const bool kWaves = getenv("AS_WAVES") ? atoi(getenv("AS_WAVES")) != 0 : true;
+  if (kWaves && nb > wave) nb = (nb + wave - 1) / wave * wave;  // below one wave: fewer, fuller tiles
+  nb = std::max(nb, (n_cols + kMaxBucketCols - 1) / kMaxBucketCols);
+  nb = std::min(nb, std::max(1ll, n_cols));
+  nb = std::min(nb, (long long)kMaxCoarse);
+  if (n_cols > 0 && (n_cols + nb - 1) / nb > kMaxBucketCols) return 0;
+  return std::max(1ll, nb);
 }
 
 // pre = true: the input arrives bucketed by column (run_persist_ws pre_ptr);
 // buckets are then variable-width (kPreT), with no column-count limit.
 static size_t carve_persist(Carve& c, PersistWs* w, long long n, long long n_cols, size_t val_bytes,
                             bool pre = false) {
+  w->cb_mul = 0;
+  w->ok = true;
   if (pre) {
-    w->wbits = 0;
     w->n_cb = (n + kPreColCost * n_cols) / kPreT + 1;
   } else {
-    w->wbits = choose_wbits(n, n_cols);
-    const int wb = w->wbits < 0 ? 10 : w->wbits;
-    w->n_cb = (n_cols + (1ll << wb) - 1) >> wb;
+    w->n_cb = choose_ncb(n, n_cols);
+    w->ok = w->n_cb > 0;
+    if (!w->ok) w->n_cb = 1;
+    // floor(2^32 * n_cb / n_cols): bucket(n_cols - 1) < n_cb
+    w->cb_mul = n_cols > 0 ? (unsigned long long)((((unsigned __int128)w->n_cb) << 32) / (unsigned long long)n_cols) : 0;
   }
   w->zero = c.take<unsigned>(64);
   w->cb_cnt = c.take<unsigned>(std::max(1ll, w->n_cb));  // pre: size class and slot of each bucket
   w->zero_bytes = c.off;
   w->cb_start = c.take<long long>(w->n_cb + 1);
-  w->cb_col = pre ? c.take<unsigned>(w->n_cb + 1) : nullptr;
+  w->cb_col = c.take<unsigned>(w->n_cb + 1);
   w->order = pre ? c.take<unsigned>(w->n_cb) : nullptr;
   const long long n1 = std::max(1ll, n);
   w->keys = c.take<unsigned long long>(n1);
@@ -103,8 +116,8 @@ template <class T, class S1, class S2>
 static int run_persist_ws(PersistWs& w, const S1& s1, const S2& s2, long long n, long long n_cols, int row_bits,
                           int mode, int prune, ValSrc<T> vs, int* col_ptr, int* row_idx, T* out_vals,
                           long long* info, bool init_info, const long long* pre_ptr, cudaStream_t st) {
-  AS_REQUIRE(w.wbits >= 0, AS_ERR_ARG, "%lld output columns exceed the %lld supported by the bucket kernel",
-             n_cols, (long long)kMaxCoarse * kMaxW);
+  AS_REQUIRE(w.ok, AS_ERR_ARG, "%lld output columns exceed the %lld supported by the bucket kernel", n_cols,
+             (long long)kMaxCoarse * kMaxBucketCols);
   if (info == nullptr) info = w.own_info;
   AS_CUDA_TRY(cudaMemsetAsync(w.zero, 0, w.zero_bytes, st));
   if (init_info) AS_CUDA_TRY(cudaMemsetAsync(info, 0x7f, 2 * sizeof(long long), st));
@@ -113,7 +126,7 @@ static int run_persist_ws(PersistWs& w, const S1& s1, const S2& s2, long long n,
   a.s2 = s2;
   a.n_cols = n_cols;
   a.n_upper = n;
-  a.wbits = w.wbits;
+  a.cb_mul = w.cb_mul;
   a.n_cb = w.n_cb;
   a.cb_cnt = w.cb_cnt;
   a.cb_start = w.cb_start;
@@ -139,7 +152,7 @@ static int run_persist_ws(PersistWs& w, const S1& s1, const S2& s2, long long n,
   a.gb = GridBar{w.zero + 16, w.zero + 32};
   a.phase_ts = nullptr;
   a.pre_ptr = pre_ptr;
-  a.cb_col = pre_ptr ? w.cb_col : nullptr;
+  a.cb_col = w.cb_col;
   a.order = pre_ptr ? w.order : nullptr;
   static unsigned long long* dbg_ts = nullptr;
   const bool phase_dbg = getenv("AS_PHASE_TIMES") != nullptr;
@@ -153,13 +166,15 @@ static int run_persist_ws(PersistWs& w, const S1& s1, const S2& s2, long long n,
     unsigned long long h[16];
     AS_CUDA_TRY(cudaMemcpyAsync(h, dbg_ts, sizeof(h), cudaMemcpyDeviceToHost, st));
     AS_CUDA_TRY(cudaStreamSynchronize(st));
-    fprintf(stderr, "[phases n=%lld n_cols=%lld W=%d n_cb=%lld]", n, n_cols, pre_ptr ? -1 : 1 << w.wbits, w.n_cb);
-    for (int i = 1, last = 0; i < 16; i++)
+    fprintf(stderr, "[phases n=%lld n_cols=%lld n_cb=%lld%s]", n, n_cols, w.n_cb, pre_ptr ? " pre" : "");
+    for (int i = 1, last = 0; i < 8; i++)
       if (h[i]) {
         fprintf(stderr, " %.2f", (h[i] - h[last]) * 1e-3);
         last = i;
       }
-    fprintf(stderr, " us\n");
+    fprintf(stderr, " us; tile steps (cycles/tile: load sort reduce write)");
+    for (int i = 8; i < 12; i++) fprintf(stderr, " %.0f", (double)h[i] / (double)(w.n_cb > 0 ? w.n_cb : 1));
+    fprintf(stderr, "\n");
   }
   return rc;
 }
