@@ -401,18 +401,7 @@ __device__ long long bucket_chunk_reduce(BTileSmem<T>& S, long long b, int cm, l
                                          const unsigned long long* gk, const unsigned* gcol, unsigned col_base,
                                          VS vs, int mode, int prune, const T* vslot) {
   const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  // all value gathers of this thread issued before any is used (L2 latency
-  // once per tile, not once per position)
-  T vv[kItems];
-#pragma unroll
-  for (int q = 0; q < kItems; q++) {
-    const int p = q * kSegThreads + tid;
-    if (p < cm) vv[q] = vslot ? vslot[S.perm[p]] : vs((unsigned long long)key_idx(S.sk[p]));
-  }
-#pragma unroll
-  for (int q = 0; q < kItems; q++) {
-    const int base = q * kSegThreads;
-    if (base >= cm) break;
+  for (int base = 0; base < cm; base += nthr) {
     const int p = base + tid;
     bool head = false;
     if (p < cm) {
@@ -420,15 +409,10 @@ __device__ long long bucket_chunk_reduce(BTileSmem<T>& S, long long b, int cm, l
       const unsigned row = key_row(k), col = S.scol[p];
       if (p > 0) head = row != key_row(S.sk[p - 1]) || col != S.scol[p - 1];
       else head = (b == 0) || row != key_row(gk[b - 1]) || col != gcol[b - 1] - col_base;
+      S.u.rv[p] = vslot ? vslot[S.perm[p]] : vs((unsigned long long)key_idx(k));
     }
     const unsigned hb = __ballot_sync(0xffffffffu, head);
     if (lane == 0 && base + warp * 32 < cm) S.hbits[(base >> 5) + warp] = hb;
-  }
-  __syncthreads();  // every read of S.u (as sk2) is done before rv overwrites it
-#pragma unroll
-  for (int q = 0; q < kItems; q++) {
-    const int p = q * kSegThreads + tid;
-    if (p < cm) S.u.rv[p] = vv[q];
   }
   __syncthreads();
   const int pb = tid * kItems, pe = min(pb + kItems, cm);
@@ -904,19 +888,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
     if (m == 0) {
       for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = 0u;
     } else if (m <= kCap) {
-      long long t_last = a.phase_ts ? clock64() : 0;
-      // debug (AS_PHASE_TIMES): cycles of each tile step summed over all tiles
-      auto tile_mark = [&](int k) {
-        if (a.phase_ts) {
-          __syncthreads();
-          if (tid == 0) {
-            const long long now = clock64();
-            atomicAdd(&a.phase_ts[8 + k], (unsigned long long)(now - t_last));
-            t_last = now;
-          }
-        }
-      };
-      {
+      {  // all loads of this thread in flight before the first store
         unsigned long long kk[kItems];
         unsigned cc[kItems];
 #pragma unroll
@@ -938,11 +910,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
         }
       }
       __syncthreads();
-      tile_mark(0);
       sort_bucket_smem(S, (int)m, Wt, a.row_bits);
-      tile_mark(1);
       bucket_chunk_reduce<T>(S, 0, (int)m, m, nullptr, nullptr, col_base, a.vs, a.mode, a.prune, a.vals_b + s);
-      tile_mark(2);
       for (int p = tid; p < m; p += nthr) {
         const unsigned e0 = S.v.excl[p], e1 = S.v.excl[p + 1];
         if (e1 != e0) {
@@ -951,7 +920,6 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
         }
       }
       for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = S.v.excl[S.cstart[l + 1]] - S.v.excl[S.cstart[l]];
-      tile_mark(3);
     } else {
       process_oversized_bucket<T>(S, a, s, m, col_base, Wt);
     }

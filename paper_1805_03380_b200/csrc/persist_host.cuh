@@ -167,14 +167,12 @@ static int run_persist_ws(PersistWs& w, const S1& s1, const S2& s2, long long n,
     AS_CUDA_TRY(cudaMemcpyAsync(h, dbg_ts, sizeof(h), cudaMemcpyDeviceToHost, st));
     AS_CUDA_TRY(cudaStreamSynchronize(st));
     fprintf(stderr, "[phases n=%lld n_cols=%lld n_cb=%lld%s]", n, n_cols, w.n_cb, pre_ptr ? " pre" : "");
-    for (int i = 1, last = 0; i < 8; i++)
+    for (int i = 1, last = 0; i < 16; i++)
       if (h[i]) {
         fprintf(stderr, " %.2f", (h[i] - h[last]) * 1e-3);
         last = i;
       }
-    fprintf(stderr, " us; tile steps (cycles/tile: load sort reduce write)");
-    for (int i = 8; i < 12; i++) fprintf(stderr, " %.0f", (double)h[i] / (double)(w.n_cb > 0 ? w.n_cb : 1));
-    fprintf(stderr, "\n");
+    fprintf(stderr, " us\n");
   }
   return rc;
 }
