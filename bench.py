@@ -169,7 +169,7 @@ def main_device(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or args.mg:
         dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -299,8 +299,11 @@ def main_device(args):
 
     # ------------------------------------------------------------ other hot-path ops (rank 0)
     ops = {}
-    if rank == 0 and not args.headline_only:
+    if rank == 0 and world == 1 and not args.headline_only:
         ops = bench_ops(args, dev, L, sp, timed, peak)
+    ops_mg = None
+    if (world > 1 or args.mg) and not args.headline_only:
+        ops_mg = bench_mg_ops(args, dev, world, rank, l2_flush, peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -324,9 +327,10 @@ def main_device(args):
                          "kernel": "as_coo_to_csc_f64 (one persistent cooperative kernel + 2 memsets)",
                          "algorithmic_bytes": build_bytes},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 1 * args.steps, "clocks": clocks, "ops": ops,
+            "ops_multi_gpu": ops_mg,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or args.mg:
         dist.barrier()
         dist.destroy_process_group()
     return 0
@@ -351,6 +355,105 @@ _TRAFFIC, TRAFFIC_SRC = _load_traffic()
 def ncu_traffic(op):
     k = _TRAFFIC.get(op)
     return None if k is None else k["dram_read"] + k["dram_write"]
+
+
+def bench_mg_ops(args, dev, world, rank, l2_flush, peak):
+    """the column-sharded trace (cfg 4), SpMM (cfg 3) and SpGEMM
+    (cfg 5) across the torchrun ranks (NCCL).  Every rank builds the same
+    seeded inputs, computes its shard with the GPU kernels and takes part in
+    the exchange; per step the rank-local kernel time and the collective time
+    are measured with CUDA events (L2 flushed first) and the max over ranks is
+    reported.  Throughput = the whole job's work / the slowest rank's time."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1805_03380_b200 import _kernels, synth
+    from paper_1805_03380_b200 import dist as D
+
+    K, W = max(3, args.op_steps // 2), args.warmup
+    out = {"ranks": world, "collective": "NCCL all_gather (torch.distributed)"}
+
+    def T(a, dt):
+        return torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
+
+    def timed_pair(local_fn, exch_fn):
+        for _ in range(W):
+            exch_fn(local_fn())
+        torch.cuda.synchronize()
+        dist.barrier()
+        loc, col = [], []
+        for _ in range(K):
+            l2_flush()
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record()
+            res = local_fn()
+            e1.record()
+            exch_fn(res)
+            e2.record()
+            torch.cuda.synchronize()
+            loc.append(e0.elapsed_time(e1))
+            col.append(e1.elapsed_time(e2))
+        t = torch.tensor([statistics.median(loc), statistics.median(col),
+                          statistics.median([x + y for x, y in zip(loc, col)])], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(x) for x in t.tolist()]
+
+    def guarded(name, fn):
+        try:
+            out[name] = fn()
+        except Exception as e:  # keep the headline line even if one sharded op fails
+            out[name] = {"error": "%s: %s" % (type(e).__name__, str(e)[:300])}
+
+    def trace_op():
+        n, _, A, B = synth.cfg4_trace_pair()
+        a = (T(A[2], torch.int32), T(A[1], torch.int32), T(A[0], torch.float64))
+        b = (T(B[2], torch.int32), T(B[1], torch.int32), T(B[0], torch.float64))
+        c0, c1, sa, sb = D.trace_shard(a, b)
+        box = {}
+
+        def exch(part):
+            box["t"] = D.trace_exchange(part)
+
+        lk, ck, tk = timed_pair(lambda: _kernels.fused_trace(n, c1 - c0, sa, sb), exch)
+        want = float(_kernels.fused_trace(n, n, a, b).cpu()[0])
+        nnz = int(A[1].shape[0] + B[1].shape[0])
+        return {"ms_local": lk, "ms_collective": ck, "ms": tk, "value": nnz / (tk * 1e-3), "unit": "nnz/s",
+                "parity": "within 1e-12 of the 1-GPU kernel (|d|=%.3g)" % abs(box["t"] - want),
+                "ok": abs(box["t"] - want) <= 1e-12 * max(1.0, abs(want))}
+
+    def spmm_op():
+        n, _, av, ar, ao, B = synth.cfg3_spmm()
+        k = B.shape[1]
+        csr = _kernels.transpose(n, n, T(ao, torch.int32), T(ar, torch.int32), T(av, torch.float32))
+        Bd = torch.as_tensor(B.T.copy(), device=dev).t()
+        k0, k1, bounds = D.spmm_block(k)
+        Xb = Bd[:, k0:k1]
+        lk, ck, tk = timed_pair(lambda: _kernels.spmm(n, n, csr, Xb), lambda blk: D.spmm_exchange(blk, bounds, n))
+        alg = 4 * (n + 1) + 8 * av.shape[0] + 8 * n * k
+        return {"ms_local": lk, "ms_collective": ck, "ms": tk, "unit": "GB/s",
+                "value_compute": alg / (lk * 1e-3) / 1e9, "value": alg / (tk * 1e-3) / 1e9,
+                "note": "A replicated, dense columns split %s; C blocks all-gathered to every rank"
+                        % [int(x) for x in bounds]}
+
+    def spgemm_op():
+        n, _, A, B = synth.cfg5_pair()
+        a = (T(A[2], torch.int32), T(A[1], torch.int32), T(A[0], torch.float64))
+        b = (T(B[2], torch.int32), T(B[1], torch.int32), T(B[0], torch.float64))
+        c0, c1, bounds, sb = D.spgemm_shard(a, b)
+        total = int(D.spgemm_column_weights(A[2], B[2], B[1]).sum())
+        lk, ck, tk = timed_pair(lambda: _kernels.spgemm(n, n, c1 - c0, a, sb),
+                                lambda res: D.spgemm_exchange(*res, bounds))
+        return {"ms_local": lk, "ms_collective": ck, "ms": tk, "value": total / (tk * 1e-3), "unit": "products/s",
+                "value_compute": total / (lk * 1e-3), "note": "B split into %d equal-product column ranges" % world}
+
+    want = set(args.ops.split(","))
+    if "trace" in want:
+        guarded("trace_cfg4", trace_op)
+    if "spmm" in want:
+        guarded("spmm_cfg3", spmm_op)
+    if "spgemm" in want:
+        guarded("spgemm_cfg5", spgemm_op)
+    return out if rank == 0 else None
 
 
 def bench_ops(args, dev, L, sp, timed, peak):
@@ -576,6 +679,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--skip-slow-checks", action="store_true")
     ap.add_argument("--flush", default="read", choices=["read", "write"])
+    ap.add_argument("--mg", action="store_true",
+                    help="run the sharded (multi-GPU) ops even at world size 1 (needs torchrun env)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -88,13 +88,51 @@ def dd_combine(parts: Sequence[Sequence[float]]) -> float:
 
 
 # ---------------------------------------------------------------------------
+# helpers
+
+def comm_device(group=None) -> torch.device:
+    """Device the collectives run on: the rank's GPU under NCCL, else CPU."""
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def _host(x) -> np.ndarray:
+    return x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+
+
+def _tensor(x, device) -> torch.Tensor:
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+    return t.to(device)
+
+
+# ---------------------------------------------------------------------------
 # trace(A^T B)
 
 def _gpu_trace_local(n_rows, n_cols, a, b):
     from . import _kernels
 
-    out = _kernels.fused_trace(n_rows, n_cols, a, b)
-    return out.cpu().tolist()
+    return _kernels.fused_trace(n_rows, n_cols, a, b)  # device f64[2] (hi, lo), no sync
+
+
+def trace_shard(a, b, group=None):
+    """This rank's column range and the (col_ptr, row_idx, vals) slices of A
+    and B, balanced on nnz(A[:,j]) + nnz(B[:,j])."""
+    rank, world = _rank_world(group)
+    weights = np.diff(_host(a[0]).astype(np.int64)) + np.diff(_host(b[0]).astype(np.int64))
+    bounds = split_by_weight(weights, world)
+    c0, c1 = int(bounds[rank]), int(bounds[rank + 1])
+    return c0, c1, csc_column_slice(*a, c0, c1), csc_column_slice(*b, c0, c1)
+
+
+def trace_exchange(part, group=None) -> float:
+    """One all_gather of every rank's (hi, lo) partial, combined in rank order."""
+    _, world = _rank_world(group)
+    mine = _tensor(np.asarray(part, dtype=np.float64) if not isinstance(part, torch.Tensor) else part,
+                   comm_device(group)).to(torch.float64).reshape(2)
+    gathered = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(gathered, mine, group=group)
+    return dd_combine([g.cpu().tolist() for g in gathered])
 
 
 def dist_fused_trace(n_rows: int, n_cols: int, a, b, group=None,
@@ -102,21 +140,8 @@ def dist_fused_trace(n_rows: int, n_cols: int, a, b, group=None,
     """trace(A^T B) over column shards.  `a`, `b`: full (col_ptr, row_idx,
     vals) on every rank (or at least their column slices' inputs)."""
     local = local or _gpu_trace_local
-    rank, world = _rank_world(group)
-    a_ptr = a[0].cpu().numpy() if isinstance(a[0], torch.Tensor) else np.asarray(a[0])
-    b_ptr = b[0].cpu().numpy() if isinstance(b[0], torch.Tensor) else np.asarray(b[0])
-    weights = np.diff(a_ptr) + np.diff(b_ptr)
-    bounds = split_by_weight(weights, world)
-    c0, c1 = int(bounds[rank]), int(bounds[rank + 1])
-    sa = csc_column_slice(*a, c0, c1)
-    sb = csc_column_slice(*b, c0, c1)
-    hi_lo = local(n_rows, c1 - c0, sa, sb)
-    mine = torch.tensor(hi_lo, dtype=torch.float64)
-    if dist.get_backend(group) == "nccl":
-        mine = mine.cuda()
-    gathered = [torch.empty_like(mine) for _ in range(world)]
-    dist.all_gather(gathered, mine, group=group)
-    return dd_combine([g.cpu().tolist() for g in gathered])
+    c0, c1, sa, sb = trace_shard(a, b, group)
+    return trace_exchange(local(n_rows, c1 - c0, sa, sb), group)
 
 
 # ---------------------------------------------------------------------------
@@ -128,27 +153,37 @@ def _gpu_spmm_local(n_rows, n_cols, csr, X):
     return _kernels.spmm(n_rows, n_cols, csr, X)
 
 
+def spmm_block(k: int, group=None):
+    """This rank's contiguous block [k0, k1) of the k dense columns."""
+    rank, world = _rank_world(group)
+    bounds = split_by_weight(np.ones(k, np.int64), world)
+    return int(bounds[rank]), int(bounds[rank + 1]), bounds
+
+
+def spmm_exchange(block, bounds, n_rows: int, group=None) -> torch.Tensor:
+    """all_gather of the column blocks (padded to the widest) -> full C."""
+    _, world = _rank_world(group)
+    tb = _tensor(block, comm_device(group))
+    if world == 1:
+        return tb
+    width = int(max(bounds[1:] - bounds[:-1]))
+    pad = torch.zeros((n_rows, width), dtype=tb.dtype, device=tb.device)
+    pad[:, : tb.shape[1]] = tb
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad.contiguous(), group=group)
+    return torch.cat([parts[r][:, : int(bounds[r + 1] - bounds[r])] for r in range(world)], dim=1)
+
+
 def dist_spmm(n_rows: int, n_cols: int, csr, X, group=None, gather: bool = True,
               local: Optional[Callable] = None):
     """Each rank computes C[:, k0:k1] for its block of dense columns.
     Returns the full C (gather=True) or (k0, k1, C_block)."""
     local = local or _gpu_spmm_local
-    rank, world = _rank_world(group)
-    k = int(X.shape[1])
-    bounds = split_by_weight(np.ones(k, np.int64), world)
-    k0, k1 = int(bounds[rank]), int(bounds[rank + 1])
+    k0, k1, bounds = spmm_block(int(X.shape[1]), group)
     block = local(n_rows, n_cols, csr, X[:, k0:k1])
     if not gather:
         return k0, k1, block
-    # all_gather of column blocks (pad to the largest block)
-    width = int(max(bounds[1:] - bounds[:-1]))
-    tb = torch.as_tensor(np.asarray(block) if not isinstance(block, torch.Tensor) else block)
-    pad = torch.zeros((n_rows, width), dtype=tb.dtype, device=tb.device)
-    pad[:, : k1 - k0] = tb
-    parts = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(parts, pad.contiguous(), group=group)
-    cols = [parts[r][:, : int(bounds[r + 1] - bounds[r])] for r in range(world)]
-    return torch.cat(cols, dim=1)
+    return spmm_exchange(block, bounds, n_rows, group)
 
 
 # ---------------------------------------------------------------------------
@@ -166,51 +201,64 @@ def spgemm_column_weights(a_ptr, b_ptr, b_rows) -> np.ndarray:
 def _gpu_spgemm_local(n_rows_a, n_inner, n_cols_b, a, b):
     from . import _kernels
 
-    p, r, v = _kernels.spgemm(n_rows_a, n_inner, n_cols_b, a, b)
-    return p.cpu().numpy(), r.cpu().numpy(), v.cpu().numpy()
+    return _kernels.spgemm(n_rows_a, n_inner, n_cols_b, a, b)  # device CSC slice
 
 
-def dist_spgemm(n_rows_a: int, n_inner: int, n_cols_b: int, a, b, group=None,
-                local: Optional[Callable] = None):
-    """C = A B with B's columns split into equal-product ranges; returns the
-    full C on every rank as host arrays (col_ptr int64, rows, vals)."""
-    local = local or _gpu_spgemm_local
+def spgemm_shard(a, b, group=None):
+    """This rank's range of B's columns (equal Gustavson products) and B's slice."""
     rank, world = _rank_world(group)
-    to_np = lambda x: x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)  # noqa: E731
-    w = spgemm_column_weights(to_np(a[0]), to_np(b[0]), to_np(b[1]))
+    w = spgemm_column_weights(_host(a[0]), _host(b[0]), _host(b[1]))
     bounds = split_by_weight(w, world)
     c0, c1 = int(bounds[rank]), int(bounds[rank + 1])
-    sb = csc_column_slice(*b, c0, c1)
-    p, r, v = local(n_rows_a, n_inner, c1 - c0, a, sb)
-    p, r, v = np.asarray(p, np.int64), np.asarray(r, np.int64), np.asarray(v, np.float64)
-    # exchange slice sizes, then the padded slices
-    nnz = torch.tensor([r.shape[0]], dtype=torch.int64)
-    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
-    dist.all_gather(sizes, nnz, group=group)
-    sizes = [int(s.item()) for s in sizes]
+    return c0, c1, bounds, csc_column_slice(*b, c0, c1)
+
+
+def spgemm_exchange(p, r, v, bounds, group=None):
+    """Gather every rank's CSC slice on the collective device: slice sizes,
+    then padded row / value / col_ptr slices; col_ptr rebased by an exclusive
+    scan of the slice nnz.  Returns (col_ptr int64, rows int64, vals f64)."""
+    _, world = _rank_world(group)
+    devc = comm_device(group)
+    p = _tensor(p, devc).to(torch.int64)
+    r = _tensor(r, devc).to(torch.int64)
+    v = _tensor(v, devc).to(torch.float64)
+    if world == 1:
+        return p, r, v
+    nnz = torch.tensor([r.shape[0]], dtype=torch.int64, device=devc)
+    sizes_t = [torch.zeros(1, dtype=torch.int64, device=devc) for _ in range(world)]
+    dist.all_gather(sizes_t, nnz, group=group)
+    sizes = [int(s.item()) for s in sizes_t]
     cap = max(1, max(sizes))
-    rows_pad = torch.zeros(cap, dtype=torch.int64)
-    vals_pad = torch.zeros(cap, dtype=torch.float64)
-    rows_pad[: r.shape[0]] = torch.from_numpy(r)
-    vals_pad[: v.shape[0]] = torch.from_numpy(v)
+    rows_pad = torch.zeros(cap, dtype=torch.int64, device=devc)
+    vals_pad = torch.zeros(cap, dtype=torch.float64, device=devc)
+    rows_pad[: r.shape[0]] = r
+    vals_pad[: v.shape[0]] = v
     all_rows = [torch.empty_like(rows_pad) for _ in range(world)]
     all_vals = [torch.empty_like(vals_pad) for _ in range(world)]
     dist.all_gather(all_rows, rows_pad, group=group)
     dist.all_gather(all_vals, vals_pad, group=group)
-    # col_ptr slices have different lengths: pad to the widest
     wmax = int(max(bounds[1:] - bounds[:-1])) + 1
-    ptr_pad = torch.zeros(wmax, dtype=torch.int64)
-    ptr_pad[: p.shape[0]] = torch.from_numpy(p)
+    ptr_pad = torch.zeros(wmax, dtype=torch.int64, device=devc)
+    ptr_pad[: p.shape[0]] = p
     all_ptr = [torch.empty_like(ptr_pad) for _ in range(world)]
     dist.all_gather(all_ptr, ptr_pad, group=group)
-    col_ptr = [np.zeros(1, np.int64)]
+    col_ptr = [torch.zeros(1, dtype=torch.int64, device=devc)]
     base = 0
-    rows_out, vals_out = [], []
     for q in range(world):
         width = int(bounds[q + 1] - bounds[q])
-        pq = all_ptr[q][: width + 1].numpy()
-        col_ptr.append(pq[1:] + base)
-        rows_out.append(all_rows[q][: sizes[q]].numpy())
-        vals_out.append(all_vals[q][: sizes[q]].numpy())
+        col_ptr.append(all_ptr[q][1: width + 1] + base)
         base += sizes[q]
-    return np.concatenate(col_ptr), np.concatenate(rows_out), np.concatenate(vals_out)
+    return (torch.cat(col_ptr), torch.cat([all_rows[q][: sizes[q]] for q in range(world)]),
+            torch.cat([all_vals[q][: sizes[q]] for q in range(world)]))
+
+
+def dist_spgemm(n_rows_a: int, n_inner: int, n_cols_b: int, a, b, group=None,
+                local: Optional[Callable] = None, on_device: bool = False):
+    """C = A B with B's columns split into equal-product ranges; returns the
+    full C on every rank: host arrays (col_ptr int64, rows int64, vals f64),
+    or tensors on the collective device with on_device=True."""
+    local = local or _gpu_spgemm_local
+    c0, c1, bounds, sb = spgemm_shard(a, b, group)
+    p, r, v = local(n_rows_a, n_inner, c1 - c0, a, sb)
+    out = spgemm_exchange(p, r, v, bounds, group)
+    return out if on_device else tuple(x.cpu().numpy() for x in out)
