@@ -19,6 +19,7 @@ LIB = os.path.join(HERE, "libbsparse.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+FLAGS += os.environ.get("AS_NVCC_EXTRA", "").split()  # experiments, e.g. -DAS_SPMM_KC=8
 
 
 def sources():

@@ -24,6 +24,9 @@
 namespace as {
 
 constexpr int kMmThreads = 256;
+#ifndef AS_SPMM_KC
+#define AS_SPMM_KC 16
+#endif
 
 // L2 eviction-priority policy for the dense chunk: written by the transpose
 // and gathered ~nnz/n_cols times by the row kernel, it must outlive the
@@ -269,7 +272,7 @@ size_t as_spmm_workspace_bytes(int64_t n_cols, int64_t k, int dtype_bytes) {
   // one row-major chunk of B: n_cols x 64 bytes
   (void)k;
   (void)dtype_bytes;
-  return (size_t)(n_cols > 0 ? n_cols : 1) * 64 + 256;
+  return (size_t)(n_cols > 0 ? n_cols : 1) * (AS_SPMM_KC * 4 > 64 ? AS_SPMM_KC * 4 : 64) + 256;
 }
 
 int as_spmm_csr_f32(int64_t n_rows, int64_t n_cols, int64_t k, const int32_t* row_ptr, const int32_t* col_idx,
@@ -286,8 +289,8 @@ int as_spmm_csr_f32(int64_t n_rows, int64_t n_cols, int64_t k, const int32_t* ro
     AS_LAUNCH_CHECK();
     return AS_OK;
   }
-  if (exact) return spmm_impl<float, 16, true>(n_rows, n_cols, k, row_ptr, col_idx, vals, B, ldb, C, ldc, (float*)ws, st);
-  return spmm_impl<float, 16, false>(n_rows, n_cols, k, row_ptr, col_idx, vals, B, ldb, C, ldc, (float*)ws, st);
+  if (exact) return spmm_impl<float, AS_SPMM_KC, true>(n_rows, n_cols, k, row_ptr, col_idx, vals, B, ldb, C, ldc, (float*)ws, st);
+  return spmm_impl<float, AS_SPMM_KC, false>(n_rows, n_cols, k, row_ptr, col_idx, vals, B, ldb, C, ldc, (float*)ws, st);
 }
 
 int as_spmm_csr_f64(int64_t n_rows, int64_t n_cols, int64_t k, const int32_t* row_ptr, const int32_t* col_idx,
