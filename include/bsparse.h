@@ -157,6 +157,47 @@ int as_trace_atb_f64(int64_t n_rows, int64_t n_cols, const int32_t *a_col_ptr, c
                      const double *b_vals, int64_t nnz_a, int64_t nnz_b, double *out, void *ws,
                      size_t ws_bytes, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * construction-funnelled ops and segmented reductions of the
+ * reference's ops module (csrc/funnel.cu).
+ *
+ * as_expand_cols: column index of every CSC element (CscData.expand_cols).
+ * as_kron_triplets_f64 / as_repmat_triplets_f64: the triplets ops.kron
+ *   (ops.py:131-143) / ops.repmat (ops.py:146-163) hand to canonicalize, in
+ *   the same order; the caller funnels them through as_coo_to_csc_f64.
+ * as_segment_reduce_f64: per segment (CSC column, or CSR row) kind 0 = the
+ *   sequential fold of np.add.at (ops.py:182-185), 1 / 2 = min / max with the
+ *   implicit zero of a non-dense slice (ops.py:186-193), 3 = max of an
+ *   empty-safe |x| (norms); xf transforms each value first (0 x, 1 |x|,
+ *   2 x*x, 3 |x|**p).  full = the slice length (rows for columns).
+ * as_pairwise_sum_f64: np.sum's pairwise summation of (transformed) x in its
+ *   exact association order (trace, norms: ops.py:209-248); out[0].
+ * as_csc_window_f64: ops.submat (ops.py:277-298) rows [r0,r1] x cols [c0,c1];
+ *   outputs sized for the window's nnz bound, info[0] = nnz.
+ * as_csc_diag_f64: ops.diag (ops.py:345-355), diagonal k as a dense vector.
+ * as_scale_by_label_f64: out = vals / norms[labels] (0 norms count as 1),
+ *   ops.normalise (ops.py:251-274) before its re-canonicalisation.
+ */
+int as_expand_cols(int64_t n_cols, const int32_t *col_ptr, int32_t *cols, void *stream);
+int as_kron_triplets_f64(int64_t nnz_a, const int32_t *a_rows, const int32_t *a_cols, const double *a_vals,
+                         int64_t nnz_b, const int32_t *b_rows, const int32_t *b_cols, const double *b_vals,
+                         int64_t b_n_rows, int64_t b_n_cols, int32_t *rows, int32_t *cols, double *vals,
+                         void *stream);
+int as_repmat_triplets_f64(int64_t nnz, const int32_t *a_rows, const int32_t *a_cols, const double *a_vals,
+                           int64_t n_rows, int64_t n_cols, int64_t reps_r, int64_t reps_c, int32_t *rows,
+                           int32_t *cols, double *vals, void *stream);
+int as_segment_reduce_f64(int64_t n_seg, const int32_t *seg_ptr, const double *vals, int kind, int xf, double p,
+                          int64_t full, double *out, void *stream);
+int as_pairwise_sum_f64(int64_t n, const double *x, int xf, double p, double *out, void *stream);
+size_t as_window_workspace_bytes(int64_t n_out_cols);
+int as_csc_window_f64(int64_t n_rows, int64_t n_cols, const int32_t *col_ptr, const int32_t *row_idx,
+                      const double *vals, int64_t r0, int64_t r1, int64_t c0, int64_t c1, int32_t *out_col_ptr,
+                      int32_t *out_rows, double *out_vals, int64_t *info, void *ws, size_t ws_bytes, void *stream);
+int as_csc_diag_f64(int64_t n_rows, int64_t n_cols, const int32_t *col_ptr, const int32_t *row_idx,
+                    const double *vals, int64_t k, int64_t length, double *out, void *stream);
+int as_scale_by_label_f64(int64_t nnz, const int32_t *labels, const double *vals, const double *norms, double *out,
+                          void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -216,3 +216,94 @@ def fused_trace(n_rows, n_cols, a, b, out=None):
     check(L.as_trace_atb_f64(n_rows, n_cols, ptr(a_ptr), ptr(a_rows), ptr(a_vals), ptr(b_ptr), ptr(b_rows),
                              ptr(b_vals), na, nb, ptr(out), ptr(ws), ws_bytes, stream()))
     return out
+
+
+# ---------------------------------------------------------------------------
+# construction-funnelled ops and segmented reductions (funnel.cu)
+
+XF_ID, XF_ABS, XF_SQUARE, XF_POW = 0, 1, 2, 3
+RED_SUM, RED_MIN, RED_MAX, RED_MAXABS = 0, 1, 2, 3
+
+
+def expand_cols(n_cols, col_ptr, nnz):
+    """Column index of every element of a CSC (int32, device)."""
+    out = torch.empty(max(nnz, 1), dtype=torch.int32, device=col_ptr.device)
+    check(_lib.lib().as_expand_cols(n_cols, ptr(col_ptr), ptr(out), stream()))
+    return out[:nnz]
+
+
+def kron_triplets(a, a_cols, b, b_cols, b_n_rows, b_n_cols):
+    """(rows, cols, vals) of ops.kron (ops.py:131-143) in the reference's order."""
+    (_, ar, av), (_, br, bv) = a, b
+    na, nb = int(ar.shape[0]), int(br.shape[0])
+    dev = ar.device
+    n = na * nb
+    rows = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    cols = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    vals = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    check(_lib.lib().as_kron_triplets_f64(na, ptr(ar), ptr(a_cols), ptr(av), nb, ptr(br), ptr(b_cols), ptr(bv),
+                                          b_n_rows, b_n_cols, ptr(rows), ptr(cols), ptr(vals), stream()))
+    return rows[:n], cols[:n], vals[:n]
+
+
+def repmat_triplets(a, a_cols, n_rows, n_cols, reps_r, reps_c):
+    """(rows, cols, vals) of ops.repmat (ops.py:146-163) in the reference's order."""
+    _, ar, av = a
+    nnz = int(ar.shape[0])
+    dev = ar.device
+    n = nnz * reps_r * reps_c
+    rows = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    cols = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    vals = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    check(_lib.lib().as_repmat_triplets_f64(nnz, ptr(ar), ptr(a_cols), ptr(av), n_rows, n_cols, reps_r, reps_c,
+                                            ptr(rows), ptr(cols), ptr(vals), stream()))
+    return rows[:n], cols[:n], vals[:n]
+
+
+def segment_reduce(seg_ptr, vals, kind, full, xf=XF_ID, p=1.0):
+    """Per-segment fold (np.add.at order) / min / max with the implicit-zero rule."""
+    n_seg = int(seg_ptr.shape[0]) - 1
+    out = torch.empty(max(n_seg, 1), dtype=torch.float64, device=seg_ptr.device)
+    check(_lib.lib().as_segment_reduce_f64(n_seg, ptr(seg_ptr), ptr(vals), kind, xf, float(p), full, ptr(out),
+                                           stream()))
+    return out[:n_seg]
+
+
+def pairwise_sum(x, xf=XF_ID, p=1.0):
+    """np.sum of (transformed) x in numpy's pairwise order; device scalar."""
+    out = torch.empty(1, dtype=torch.float64, device=x.device)
+    check(_lib.lib().as_pairwise_sum_f64(int(x.shape[0]), ptr(x), xf, float(p), ptr(out), stream()))
+    return out
+
+
+def csc_window(n_rows, n_cols, csc, r0, r1, c0, c1):
+    """Rows [r0, r1] x cols [c0, c1] of a CSC, re-indexed to the origin."""
+    L = _lib.lib()
+    p, r, v = csc
+    dev = p.device
+    nc = c1 - c0 + 1
+    cap = max(int(r.shape[0]), 1)
+    out_p = torch.empty(nc + 1, dtype=torch.int32, device=dev)
+    out_r = torch.empty(cap, dtype=torch.int32, device=dev)
+    out_v = torch.empty(cap, dtype=torch.float64, device=dev)
+    info = torch.zeros(2, dtype=torch.int64, device=dev)
+    wb = L.as_window_workspace_bytes(nc)
+    ws = workspace(wb, dev)
+    check(L.as_csc_window_f64(n_rows, n_cols, ptr(p), ptr(r), ptr(v), r0, r1, c0, c1, ptr(out_p), ptr(out_r),
+                              ptr(out_v), ptr(info), ptr(ws), wb, stream()))
+    nnz = int(info[0].item())
+    return out_p, out_r[:nnz], out_v[:nnz]
+
+
+def csc_diag(n_rows, n_cols, csc, k, length):
+    p, r, v = csc
+    out = torch.empty(max(length, 1), dtype=torch.float64, device=p.device)
+    check(_lib.lib().as_csc_diag_f64(n_rows, n_cols, ptr(p), ptr(r), ptr(v), k, length, ptr(out), stream()))
+    return out[:length]
+
+
+def scale_by_label(labels, vals, norms):
+    out = torch.empty_like(vals)
+    check(_lib.lib().as_scale_by_label_f64(int(vals.shape[0]), ptr(labels), ptr(vals), ptr(norms), ptr(out),
+                                           stream()))
+    return out

@@ -48,6 +48,15 @@ SIGNATURES = {
     "as_vecmat_csc_f64": (INT, [I64, I64, P, P, P, P, P, P]),
     "as_trace_workspace_bytes": (SZ, [I64, I64, I64]),
     "as_trace_atb_f64": (INT, [I64, I64, P, P, P, P, P, P, I64, I64, P, P, SZ, P]),
+    "as_expand_cols": (INT, [I64, P, P, P]),
+    "as_kron_triplets_f64": (INT, [I64, P, P, P, I64, P, P, P, I64, I64, P, P, P, P]),
+    "as_repmat_triplets_f64": (INT, [I64, P, P, P, I64, I64, I64, I64, P, P, P, P]),
+    "as_segment_reduce_f64": (INT, [I64, P, P, INT, INT, DBL, I64, P, P]),
+    "as_pairwise_sum_f64": (INT, [I64, P, INT, DBL, P, P]),
+    "as_window_workspace_bytes": (SZ, [I64]),
+    "as_csc_window_f64": (INT, [I64, I64, P, P, P, I64, I64, I64, I64, P, P, P, P, P, SZ, P]),
+    "as_csc_diag_f64": (INT, [I64, I64, P, P, P, I64, I64, P, P]),
+    "as_scale_by_label_f64": (INT, [I64, P, P, P, P, P]),
 }
 
 AS_OK, AS_ERR_SHAPE, AS_ERR_COORD, AS_ERR_CORRUPT, AS_ERR_CUDA, AS_ERR_ARG = range(6)

@@ -241,16 +241,88 @@ def gen_trace(rng):
     save("trace", cases)
 
 
-def main():
-    rng = np.random.default_rng(20260809)
-    gen_canonicalize(rng)
-    gen_flush(rng)
-    gen_transpose(rng)
-    gen_linear_combine(rng)
-    gen_spgemm(rng)
-    gen_spmv(rng)
-    gen_trace(rng)
+def _mat(A, r, c):
+    return SpMat.from_csc(csc.CscData(Dims(r, c), A[0], A[1], A[2]))
+
+
+def _csc_out(m):
+    d = m.csc()
+    return d.values, d.row_indices, d.col_offsets
+
+
+def gen_funnel(rng):
+    """construction-funnelled ops and segmented reductions
+    (ops.py:131-163, 166-212, 228-298, 345-355)."""
+    cases = []
+
+    def mk(r, c, n, lo=-1.0, hi=1.0):
+        rows, cols = rng.integers(0, r, n), rng.integers(0, c, n)
+        return ref_canon(r, c, rows, cols, rng.uniform(lo, hi, n), "sum")
+
+    # kron (incl. an underflow of a product to exact zero, pruned by canonicalize)
+    for (ar, ac, na, br, bc, nb) in [(3, 4, 6, 2, 5, 4), (20, 15, 60, 13, 17, 50), (1, 1, 1, 40, 30, 200),
+                                     (50, 40, 300, 30, 20, 150)]:
+        A, B = mk(ar, ac, na), mk(br, bc, nb)
+        o = _csc_out(ops.kron(_mat(A, ar, ac), _mat(B, br, bc)))
+        cases.append(dict(op="kron", ar=ar, ac=ac, br=br, bc=bc, a_vals=A[0], a_rows=A[1], a_offs=A[2],
+                          b_vals=B[0], b_rows=B[1], b_offs=B[2], out_vals=o[0], out_rows=o[1], out_offs=o[2]))
+    A = ref_canon(2, 2, np.array([0, 1]), np.array([0, 1]), np.array([1e-200, 3.0]), "sum")
+    B = ref_canon(2, 1, np.array([0, 1]), np.array([0, 0]), np.array([1e-200, 2.0]), "sum")
+    o = _csc_out(ops.kron(_mat(A, 2, 2), _mat(B, 2, 1)))
+    cases.append(dict(op="kron", ar=2, ac=2, br=2, bc=1, a_vals=A[0], a_rows=A[1], a_offs=A[2],
+                      b_vals=B[0], b_rows=B[1], b_offs=B[2], out_vals=o[0], out_rows=o[1], out_offs=o[2]))
+    # repmat
+    for (r, c, n, rr, rc) in [(3, 4, 6, 2, 3), (30, 20, 200, 3, 1), (17, 9, 50, 1, 4), (100, 80, 1500, 2, 2)]:
+        A = mk(r, c, n)
+        o = _csc_out(ops.repmat(_mat(A, r, c), rr, rc))
+        cases.append(dict(op="repmat", r=r, c=c, reps_r=rr, reps_c=rc, a_vals=A[0], a_rows=A[1], a_offs=A[2],
+                          out_vals=o[0], out_rows=o[1], out_offs=o[2]))
+    # reductions, trace, diag, norms, normalise, submat on a few shapes
+    shapes = [(6, 5, 12), (40, 30, 400), (300, 200, 3000), (5, 5, 25), (1, 50, 30), (60, 1, 40), (3, 3, 9)]
+    for (r, c, n) in shapes:
+        A = mk(r, c, n, -2.0, 2.0)
+        M = _mat(A, r, c)
+        base = dict(r=r, c=c, a_vals=A[0], a_rows=A[1], a_offs=A[2])
+        for kind, fn in (("sum", ops.sum_dim), ("min", ops.min_dim), ("max", ops.max_dim)):
+            for dim in (0, 1):
+                cases.append(dict(base, op="reduce", kind=kind, dim=dim, out=fn(M, dim)))
+        cases.append(dict(base, op="trace", out=ops.trace(M)))
+        for k in (-2, 0, 1):
+            try:
+                cases.append(dict(base, op="diag", k=k, out=ops.diag(M, k)))
+            except Exception:
+                pass
+        vec = r == 1 or c == 1
+        for p in ((1, 2, 3, np.inf, "fro") if vec else (1, np.inf, "fro")):
+            cases.append(dict(base, op="norm", p=str(p), out=ops.norm(M, p)))
+        for p in (1, 2, 3, np.inf):
+            for dim in (0, 1):
+                o = _csc_out(ops.normalise(M, p, dim))
+                cases.append(dict(base, op="normalise", p=str(p), dim=dim, out_vals=o[0], out_rows=o[1],
+                                  out_offs=o[2]))
+        if r > 2 and c > 2:
+            for (r0, r1, c0, c1) in [(0, r - 1, 0, c - 1), (1, r // 2, 1, c // 2), (r // 2, r - 1, 0, 0)]:
+                o = _csc_out(ops.submat(M, (r0, r1), (c0, c1)))
+                cases.append(dict(base, op="submat", r0=r0, r1=r1, c0=c0, c1=c1, out_vals=o[0], out_rows=o[1],
+                                  out_offs=o[2]))
+    save("funnel", cases)
+
+
+def main(only=None):
+    """No arguments: every file.  `funnel` alone: only funnel.npz (its own
+    seed; the first seven share one generator stream in this order)."""
+    if not only or set(only) - {"funnel"}:
+        rng = np.random.default_rng(20260809)
+        gen_canonicalize(rng)
+        gen_flush(rng)
+        gen_transpose(rng)
+        gen_linear_combine(rng)
+        gen_spgemm(rng)
+        gen_spmv(rng)
+        gen_trace(rng)
+    if not only or "funnel" in only:
+        gen_funnel(np.random.default_rng(20261019))
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:] or None)

@@ -1,0 +1,135 @@
+"""SURVEY 8f-2 (the rows §8 marks "next"): the construction-funnelled ops
+and segmented reductions of the reference's ops module, through the device
+kernels of csrc/funnel.cu and the GPU build, against golden vectors produced
+by the reference itself (tests/golden/make_golden.py gen_funnel).
+
+Bit-exact wherever the reference's arithmetic is reproduced operation for
+operation (kron, repmat, reductions, trace's pairwise sum, the 1 / 2 / inf /
+"fro" norms, normalise with p in {1, 2, inf}, submat, diag); p = 3 goes
+through libm-vs-CUDA pow and is held to 1e-12."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+CASES = load_golden("funnel")
+
+
+def _ids(c):
+    extra = "".join("_%s%s" % (k, c[k]) for k in ("kind", "dim", "p", "k") if k in c)
+    return "%s_%sx%s%s" % (c["op"], c.get("r", c.get("ar")), c.get("c", c.get("ac")), extra)
+
+
+def _mat(vals, rows, offs, r, c):
+    from paper_1805_03380_b200 import SpMat
+    from paper_1805_03380_b200.csc import CscData, Dims
+
+    return SpMat.from_csc(CscData.from_reference_arrays(Dims(int(r), int(c)), vals, rows, offs, device="cuda"))
+
+
+def _out(m):
+    d = m.csc()
+    return d.values, d.row_indices, d.col_offsets
+
+
+def _p(s):
+    return {"inf": np.inf, "fro": "fro"}.get(s, None) if s in ("inf", "fro") else float(s)
+
+
+def _same_csc(got, case, exact=True):
+    v, r, o = got
+    assert np.array_equal(np.asarray(o, np.int64), case["out_offs"].astype(np.int64))
+    assert np.array_equal(np.asarray(r, np.int64), case["out_rows"].astype(np.int64))
+    if exact:
+        assert np.array_equal(np.asarray(v).view(np.int64), case["out_vals"].astype(np.float64).view(np.int64))
+    else:
+        w = case["out_vals"]
+        assert np.all(np.abs(v - w) <= 1e-12 * np.maximum(1.0, np.abs(w)))
+
+
+@pytest.mark.parametrize("case", CASES, ids=_ids)
+def test_funnel_golden(case):
+    from paper_1805_03380_b200 import ops
+
+    op = case["op"]
+    if op == "kron":
+        A = _mat(case["a_vals"], case["a_rows"], case["a_offs"], case["ar"], case["ac"])
+        B = _mat(case["b_vals"], case["b_rows"], case["b_offs"], case["br"], case["bc"])
+        _same_csc(_out(ops.kron(A, B)), case)
+        return
+    if op == "repmat":
+        A = _mat(case["a_vals"], case["a_rows"], case["a_offs"], case["r"], case["c"])
+        _same_csc(_out(ops.repmat(A, int(case["reps_r"]), int(case["reps_c"]))), case)
+        return
+    A = _mat(case["a_vals"], case["a_rows"], case["a_offs"], case["r"], case["c"])
+    if op == "reduce":
+        fn = {"sum": ops.sum_dim, "min": ops.min_dim, "max": ops.max_dim}[case["kind"]]
+        got = fn(A, int(case["dim"]))
+        assert np.array_equal(got.view(np.int64), np.asarray(case["out"], np.float64).view(np.int64))
+    elif op == "trace":
+        assert ops.trace(A) == float(case["out"])
+    elif op == "diag":
+        got = ops.diag(A, int(case["k"]))
+        assert np.array_equal(got, case["out"])
+    elif op == "norm":
+        p = _p(case["p"])
+        got = ops.norm(A, p)
+        want = float(case["out"])
+        if case["p"] in ("3", "3.0"):
+            assert abs(got - want) <= 1e-12 * max(1.0, abs(want))
+        else:
+            assert got == want
+    elif op == "normalise":
+        p = _p(case["p"])
+        _same_csc(_out(ops.normalise(A, p, int(case["dim"]))), case, exact=case["p"] not in ("3", "3.0"))
+    elif op == "submat":
+        got = ops.submat(A, (int(case["r0"]), int(case["r1"])), (int(case["c0"]), int(case["c1"])))
+        _same_csc(_out(got), case)
+    else:
+        raise AssertionError("unknown op %s" % op)
+
+
+def test_set_submat_and_set_diag_match_dense_model():
+    from paper_1805_03380_b200 import SpMat, ops
+
+    rng = np.random.default_rng(3)
+    dense = np.zeros((12, 10))
+    idx = rng.integers(0, 120, 50)
+    dense.flat[idx] = rng.uniform(-1, 1, 50)
+    a = SpMat.from_dense(dense, device="cuda")
+    src = np.zeros((4, 3))
+    src[1, 2] = 5.0
+    src[3, 0] = -2.0
+    ops.set_submat(a, (2, 5), (4, 6), SpMat.from_dense(src, device="cuda"))
+    dense[2:6, 4:7] = src
+    assert np.array_equal(a.to_dense(), dense)
+    vals = np.array([1.0, 0.0, 2.0, 3.0, 0.0, 4.0, 5.0, 6.0, 7.0])
+    ops.set_diag(a, 1, vals)
+    for t in range(9):
+        dense[t, t + 1] = vals[t]
+    assert np.array_equal(a.to_dense(), dense)
+    assert np.array_equal(ops.diag(a, 1), vals)
+
+
+def test_funnel_errors():
+    from paper_1805_03380_b200 import SpMat, ops
+    from paper_1805_03380_b200.errors import NormOrderError, ShapeError
+
+    a = SpMat.from_triplets(3, 4, [(0, 0, 1.0), (2, 3, -2.0)], device="cuda")
+    with pytest.raises(NormOrderError):
+        ops.norm(a, 2)
+    with pytest.raises(NormOrderError):
+        ops.normalise(a, 0.5)
+    with pytest.raises(ShapeError):
+        ops.repmat(a, 0, 1)
+    with pytest.raises(ShapeError):
+        ops.submat(a, (0, 3), (0, 0))
+    with pytest.raises(ShapeError):
+        ops.diag(a, 4)
+    with pytest.raises(ValueError):
+        ops.sum_dim(a, 2)
+    with pytest.raises(ShapeError):
+        ops.sum_dim(SpMat.zeros(0, 3, device="cuda"), 0)

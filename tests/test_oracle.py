@@ -87,3 +87,42 @@ def test_trace_reference_pins():
     # test_expr.py:133-150: diag(1,2) . diag(3,4) -> 11; disjoint -> 0
     assert oracle.fused_trace(2, [1.0, 2.0], [0, 1], [0, 1, 2], [3.0, 4.0], [0, 1], [0, 1, 2]) == 11.0
     assert oracle.fused_trace(3, [5.0], [0], [0, 1, 1, 1], [7.0], [1], [0, 0, 1, 1]) == 0.0
+
+
+def test_funnel_oracle_golden():
+    """oracle/funnel.py against the reference's own outputs."""
+    from oracle import funnel as F
+
+    def p_of(s):
+        return np.inf if s == "inf" else ("fro" if s == "fro" else float(s))
+
+    def same(got, c, exact=True):
+        v, r, o = got
+        assert np.array_equal(o, c["out_offs"]) and np.array_equal(r, c["out_rows"])
+        if exact:
+            assert np.array_equal(v.view(np.int64), c["out_vals"].view(np.int64))
+        else:
+            assert np.allclose(v, c["out_vals"], rtol=1e-12, atol=0)
+
+    for c in load_golden("funnel"):
+        op = c["op"]
+        if op == "kron":
+            same(F.kron((c["a_vals"], c["a_rows"], c["a_offs"]), c["ar"], c["ac"],
+                        (c["b_vals"], c["b_rows"], c["b_offs"]), c["br"], c["bc"]), c)
+            continue
+        a = (c["a_vals"], c["a_rows"], c["a_offs"])
+        if op == "repmat":
+            same(F.repmat(a, c["r"], c["c"], c["reps_r"], c["reps_c"]), c)
+        elif op == "reduce":
+            assert np.array_equal(F.reduce(a, c["r"], c["c"], c["kind"], c["dim"]).view(np.int64),
+                                  np.asarray(c["out"], np.float64).view(np.int64))
+        elif op == "trace":
+            assert F.trace(a) == float(c["out"])
+        elif op == "diag":
+            assert np.array_equal(F.diag(a, c["r"], c["c"], c["k"]), c["out"])
+        elif op == "norm":
+            assert F.norm(a, c["r"], c["c"], p_of(c["p"])) == float(c["out"])
+        elif op == "normalise":
+            same(F.normalise(a, c["r"], c["c"], p_of(c["p"]), c["dim"]), c)
+        elif op == "submat":
+            same(F.submat(a, c["r0"], c["r1"], c["c0"], c["c1"]), c)
