@@ -676,6 +676,61 @@ def bench_ops(args, dev, L, sp, timed, peak):
             record("spgemm_cfg5", timed(f, max(3, K // 4), W), total, "products/s",
                    12 * (na + nb) + 8 * (n + 1) + 12 * nnz + 4 * (n + 1), parity,
                    {"products": total, "nnz_out": nnz, "launches": 6})
+
+    # SURVEY 8f-2 ("next" rows): construction-funnelled ops and segmented
+    # reductions through the public ops API on the cfg 1 matrix (10k x 10k,
+    # 995,078 nnz), each checked against oracle/funnel.py first
+    if "next" in want_ops:
+        from oracle import funnel as OF
+        from paper_1805_03380_b200 import SpMat, ops
+        from paper_1805_03380_b200.csc import CscData, Dims
+
+        n_rows, n_cols, rows, cols, vals = synth.cfg1_triplets()
+        Am = oracle.canonicalize(n_rows, n_cols, rows, cols, vals)
+        A = SpMat.from_csc(CscData.from_reference_arrays(Dims(n_rows, n_cols), *Am, device=dev))
+        A.csr()  # the per-row reductions use the cached CSR, as every row-split op does
+        nnz = int(Am[0].shape[0])
+        small = oracle.canonicalize(40, 25, np.arange(100) % 40, np.arange(100) % 25, np.linspace(-1, 1, 100))
+        S = SpMat.from_csc(CscData.from_reference_arrays(Dims(40, 25), *small, device=dev))
+
+        def chk(name, ok):
+            if not ok:
+                raise CorrectnessError("%s differs from oracle/funnel.py" % name)
+
+        def same(m, want):
+            d = m.csc()
+            return (np.array_equal(d.col_offsets, want[2]) and np.array_equal(d.row_indices, want[1])
+                    and np.array_equal(d.values.view(np.int64), want[0].view(np.int64)))
+
+        nxt = [
+            ("sum_dim0", lambda: ops.sum_dim(A, 0),
+             lambda r: np.array_equal(r, OF.reduce(Am, n_rows, n_cols, "sum", 0)), 12 * nnz + 4 * n_cols + 8 * n_cols),
+            ("max_dim1", lambda: ops.max_dim(A, 1),
+             lambda r: np.array_equal(r, OF.reduce(Am, n_rows, n_cols, "max", 1)), 12 * nnz + 4 * n_rows + 8 * n_rows),
+            ("norm_fro", lambda: ops.norm(A, "fro"), lambda r: r == OF.norm(Am, n_rows, n_cols, "fro"), 8 * nnz),
+            ("norm_1", lambda: ops.norm(A, 1), lambda r: r == OF.norm(Am, n_rows, n_cols, 1), 8 * nnz + 4 * n_cols),
+            ("trace", lambda: ops.trace(A), lambda r: r == OF.trace(Am), 12 * nnz + 4 * n_cols),
+            ("submat", lambda: ops.submat(A, (1000, 8999), (2000, 7999)),
+             lambda r: same(r, OF.submat(Am, 1000, 8999, 2000, 7999)), 24 * nnz),
+            ("normalise_2_dim0", lambda: ops.normalise(A, 2, 0),
+             lambda r: same(r, OF.normalise(Am, n_rows, n_cols, 2, 0)), 16 * nnz + 12 * nnz + 16 * nnz),
+            ("repmat_2x2", lambda: ops.repmat(A, 2, 2),
+             lambda r: same(r, OF.repmat(Am, n_rows, n_cols, 2, 2)), 12 * nnz + 4 * 12 * nnz),
+            ("kron_small_x_cfg1", lambda: ops.kron(S, A), None, 12 * nnz * 100),
+        ]
+        res = {}
+        for name, fn, check_fn, alg in nxt:
+            r = fn()
+            torch.cuda.synchronize()
+            parity = "skipped (size)"
+            if check_fn is not None and not args.skip_slow_checks:
+                chk(name, check_fn(r))
+                parity = "bit-exact vs oracle/funnel.py"
+            ms = statistics.median(timed(fn, max(3, K // 2), W))
+            gbs = alg / (ms * 1e-3) / 1e9
+            res[name] = {"ms": ms, "GB/s": gbs, "frac": gbs / peak, "algorithmic_bytes": alg, "parity": parity,
+                         "path": "public ops API (host sync for scalar / vector results included)"}
+        out["next_8f2_cfg1"] = res
     return out
 
 
@@ -691,7 +746,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--ops", default="transpose,flush,spmm,trace,add,spgemm")
+    ap.add_argument("--ops", default="transpose,flush,spmm,trace,add,spgemm,next")
     ap.add_argument("--op-steps", type=int, default=10)
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -188,7 +188,9 @@ int as_repmat_triplets_f64(int64_t nnz, const int32_t *a_rows, const int32_t *a_
                            int32_t *cols, double *vals, void *stream);
 int as_segment_reduce_f64(int64_t n_seg, const int32_t *seg_ptr, const double *vals, int kind, int xf, double p,
                           int64_t full, double *out, void *stream);
-int as_pairwise_sum_f64(int64_t n, const double *x, int xf, double p, double *out, void *stream);
+size_t as_pairwise_workspace_bytes(void);
+int as_pairwise_sum_f64(int64_t n, const double *x, int xf, double p, double *out, void *ws, size_t ws_bytes,
+                        void *stream);
 size_t as_window_workspace_bytes(int64_t n_out_cols);
 int as_csc_window_f64(int64_t n_rows, int64_t n_cols, const int32_t *col_ptr, const int32_t *row_idx,
                       const double *vals, int64_t r0, int64_t r1, int64_t c0, int64_t c1, int32_t *out_col_ptr,

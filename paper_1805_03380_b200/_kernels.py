@@ -271,8 +271,11 @@ def segment_reduce(seg_ptr, vals, kind, full, xf=XF_ID, p=1.0):
 
 def pairwise_sum(x, xf=XF_ID, p=1.0):
     """np.sum of (transformed) x in numpy's pairwise order; device scalar."""
+    L = _lib.lib()
     out = torch.empty(1, dtype=torch.float64, device=x.device)
-    check(_lib.lib().as_pairwise_sum_f64(int(x.shape[0]), ptr(x), xf, float(p), ptr(out), stream()))
+    wb = L.as_pairwise_workspace_bytes()
+    ws = workspace(wb, x.device)
+    check(L.as_pairwise_sum_f64(int(x.shape[0]), ptr(x), xf, float(p), ptr(out), ptr(ws), wb, stream()))
     return out
 
 

@@ -52,7 +52,8 @@ SIGNATURES = {
     "as_kron_triplets_f64": (INT, [I64, P, P, P, I64, P, P, P, I64, I64, P, P, P, P]),
     "as_repmat_triplets_f64": (INT, [I64, P, P, P, I64, I64, I64, I64, P, P, P, P]),
     "as_segment_reduce_f64": (INT, [I64, P, P, INT, INT, DBL, I64, P, P]),
-    "as_pairwise_sum_f64": (INT, [I64, P, INT, DBL, P, P]),
+    "as_pairwise_workspace_bytes": (SZ, []),
+    "as_pairwise_sum_f64": (INT, [I64, P, INT, DBL, P, P, SZ, P]),
     "as_window_workspace_bytes": (SZ, [I64]),
     "as_csc_window_f64": (INT, [I64, I64, P, P, P, I64, I64, I64, I64, P, P, P, P, P, SZ, P]),
     "as_csc_diag_f64": (INT, [I64, I64, P, P, P, I64, I64, P, P]),

@@ -109,46 +109,72 @@ segment_reduce_kernel(long long n_seg, const int* __restrict__ seg_ptr, const do
 
 // numpy's pairwise summation (np.sum of a contiguous float64 array) in its
 // exact association order, in parallel: the recursion splits a range of n >
-// 128 elements at n/2 rounded down to a multiple of 8.  Thread t of one
-// 1024-thread block follows bits of t down kPwDepth levels of that tree (a
-// range <= 128 stops splitting: the leftmost thread below it owns it), sums
-// its node sequentially with the same rule (pw_sum), and the nodes are
-// combined bottom-up exactly as the recursion adds its two halves.
-constexpr int kPwThreads = 1024, kPwDepth = 10;
+// 128 elements at n/2 rounded down to a multiple of 8.  Block b of 2^top
+// follows the bits of b down the first `top` levels of that tree, then
+// thread t of its 1024 follows the bits of t down kPwDepth more (a range <=
+// 128 stops splitting: the leftmost thread below it owns it), sums its node
+// sequentially with the same rule (pw_sum), and the nodes are combined
+// bottom-up exactly as the recursion adds its two halves -- inside the block,
+// then across the blocks in a one-block pass.
+constexpr int kPwThreads = 1024, kPwDepth = 10, kPwTopMax = 6;
 
-__global__ void __launch_bounds__(kPwThreads)
-pairwise_sum_kernel(long long n, const double* __restrict__ x, int xf, double p, double* __restrict__ out) {
-  __shared__ double s[kPwThreads];
-  const int t = threadIdx.x;
-  long long lo = 0, len = n;
-  unsigned split_mask = 0;  // bit L: the node on this thread's path at level L was split
-  bool owner = true;
-  for (int L = 0; L < kPwDepth; L++) {
-    const int bit = (t >> (kPwDepth - 1 - L)) & 1;
-    if (len > 128) {
-      split_mask |= 1u << L;
-      long long n2 = len / 2;
+struct PwNode {
+  long long lo, len;
+  unsigned split;  // bit L: the node on the path at level L was split
+  bool owner;
+};
+
+// descend `levels` levels from (lo, len) following the bits of `path` (MSB first)
+AS_DEVICE_INLINE PwNode pw_descend(long long lo, long long len, unsigned path, int levels) {
+  PwNode nd{lo, len, 0u, true};
+  for (int L = 0; L < levels; L++) {
+    const unsigned bit = (path >> (levels - 1 - L)) & 1u;
+    if (nd.len > 128) {
+      nd.split |= 1u << L;
+      long long n2 = nd.len / 2;
       n2 -= n2 % 8;
       if (bit) {
-        lo += n2;
-        len -= n2;
+        nd.lo += n2;
+        nd.len -= n2;
       } else {
-        len = n2;
+        nd.len = n2;
       }
     } else if (bit) {
-      owner = false;  // below a leaf: only the leftmost descendant holds it
+      nd.owner = false;
     }
   }
+  return nd;
+}
+
+__global__ void __launch_bounds__(kPwThreads)
+pairwise_sum_kernel(long long n, const double* __restrict__ x, int xf, double p, int top, double* __restrict__ part) {
+  __shared__ double s[kPwThreads];
+  const int t = threadIdx.x;
+  const PwNode blk = pw_descend(0, n, blockIdx.x, top);
+  const PwNode nd = pw_descend(blk.lo, blk.len, (unsigned)t, kPwDepth);
   double v = 0.0;
-  if (owner && len > 0) v = pw_sum<double>([&](long long i) { return xform(__ldg(&x[lo + i]), xf, p); }, 0, len);
+  if (blk.owner && nd.owner && nd.len > 0)
+    v = pw_sum<double>([&](long long i) { return xform(__ldg(&x[nd.lo + i]), xf, p); }, 0, nd.len);
   s[t] = v;
   __syncthreads();
   for (int L = kPwDepth - 1; L >= 0; L--) {
     const int span = 1 << (kPwDepth - L);  // threads under a level-L node
-    if ((t & (span - 1)) == 0 && ((split_mask >> L) & 1u)) s[t] = __dadd_rn(s[t], s[t + span / 2]);
+    if ((t & (span - 1)) == 0 && ((nd.split >> L) & 1u)) s[t] = __dadd_rn(s[t], s[t + span / 2]);
     __syncthreads();
   }
-  if (t == 0) out[0] = s[0];
+  if (t == 0) part[blockIdx.x] = s[0];
+}
+
+__global__ void pairwise_combine_kernel(long long n, int top, double* __restrict__ part, double* __restrict__ out) {
+  const int t = threadIdx.x;  // blockDim = 2^top
+  const PwNode nd = pw_descend(0, n, (unsigned)t, top);
+  for (int L = top - 1; L >= 0; L--) {
+    const int span = 1 << (top - L);
+    __syncthreads();
+    if ((t & (span - 1)) == 0 && ((nd.split >> L) & 1u)) part[t] = __dadd_rn(part[t], part[t + span / 2]);
+  }
+  __syncthreads();
+  if (t == 0) out[0] = part[0];
 }
 
 // submat: rows [r0, r1] of columns [c0, c1]; counts via binary search
@@ -267,10 +293,19 @@ int as_segment_reduce_f64(int64_t n_seg, const int32_t* seg_ptr, const double* v
   return AS_OK;
 }
 
-int as_pairwise_sum_f64(int64_t n, const double* x, int xf, double p, double* out, void* stream) {
+size_t as_pairwise_workspace_bytes(void) { return sizeof(double) << kPwTopMax; }
+
+int as_pairwise_sum_f64(int64_t n, const double* x, int xf, double p, double* out, void* ws, size_t ws_bytes,
+                        void* stream) {
   AS_REQUIRE(n >= 0, AS_ERR_SHAPE, "negative length");
   AS_REQUIRE(xf >= 0 && xf <= 3, AS_ERR_ARG, "unknown transform %d", xf);
-  pairwise_sum_kernel<<<1, kPwThreads, 0, S(stream)>>>(n, x, xf, p, out);
+  AS_REQUIRE(ws_bytes >= as_pairwise_workspace_bytes(), AS_ERR_ARG, "workspace too small");
+  int top = 0;  // 2^top blocks of 1024 threads, >= ~64 elements per thread
+  while (top < kPwTopMax && (n >> (kPwDepth + top + 1)) >= 64) top++;
+  double* part = (double*)ws;
+  pairwise_sum_kernel<<<1u << top, kPwThreads, 0, S(stream)>>>(n, x, xf, p, top, part);
+  AS_LAUNCH_CHECK();
+  pairwise_combine_kernel<<<1, 1u << top, 0, S(stream)>>>(n, top, part, out);
   AS_LAUNCH_CHECK();
   return AS_OK;
 }
