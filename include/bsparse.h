@@ -200,6 +200,24 @@ int as_csc_diag_f64(int64_t n_rows, int64_t n_cols, const int32_t *col_ptr, cons
 int as_scale_by_label_f64(int64_t nnz, const int32_t *labels, const double *vals, const double *norms, double *out,
                           void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Matrix Market coordinate I/O (io.py:33-132), HOST functions
+ * (csrc/mmio.cu), multi-threaded; the triplets then go to as_coo_to_csc_f64.
+ * as_mm_header: header + size line; as_mm_entries: the entries as 0-based
+ *   int64 rows / cols and float64 values, validated in the reference's order
+ *   (AS_ERR_ARG = MatrixMarketError, AS_ERR_CORRUPT = CorruptionError, with
+ *   *err_line the reference's 1-based line number, as_last_error() the bare
+ *   message); as_mm_format: "%d %d %.17g" lines after the header, returns
+ *   the byte count (cap >= 64 + 72 * nnz suffices) or -1.
+ */
+int as_mm_header(const char *buf, int64_t len, int64_t *n_rows, int64_t *n_cols, int64_t *nnz, int64_t *entries_off,
+                 int64_t *entries_line, int64_t *err_line);
+int as_mm_entries(const char *buf, int64_t len, int64_t entries_off, int64_t entries_line, int64_t n_rows,
+                  int64_t n_cols, int64_t nnz, int64_t *rows, int64_t *cols, double *vals, int n_threads,
+                  int64_t *err_line);
+int64_t as_mm_format(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t *rows, const int64_t *cols,
+                     const double *vals, char *out, int64_t cap, int n_threads);
+
 #ifdef __cplusplus
 }
 #endif

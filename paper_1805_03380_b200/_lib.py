@@ -58,6 +58,9 @@ SIGNATURES = {
     "as_csc_window_f64": (INT, [I64, I64, P, P, P, I64, I64, I64, I64, P, P, P, P, P, SZ, P]),
     "as_csc_diag_f64": (INT, [I64, I64, P, P, P, I64, I64, P, P]),
     "as_scale_by_label_f64": (INT, [I64, P, P, P, P, P]),
+    "as_mm_header": (INT, [P, I64, P, P, P, P, P, P]),
+    "as_mm_entries": (INT, [P, I64, I64, I64, I64, I64, I64, P, P, P, INT, P]),
+    "as_mm_format": (I64, [I64, I64, I64, P, P, P, P, I64, INT]),
 }
 
 AS_OK, AS_ERR_SHAPE, AS_ERR_COORD, AS_ERR_CORRUPT, AS_ERR_CUDA, AS_ERR_ARG = range(6)

@@ -308,10 +308,77 @@ def gen_funnel(rng):
     save("funnel", cases)
 
 
+def gen_mm(rng):
+    """Matrix Market text -> reference load_mm outcome (the
+    canonical CSC, or the exception class and message), and reference
+    save_mm text of random matrices (io.py:33-131)."""
+    import io as _io
+
+    from autosparse import io as ref_io
+
+    H = "%%MatrixMarket matrix coordinate real general\n"
+    texts = [
+        (H + "2 2 1\n1 1 2.5\n", False),
+        (H + "% a comment\n2 2 1\n% another\n1 1 2.5\n", False),
+        (H + "2 2 1\n1 1\n", False),
+        (H + "2 2 1\n3 1 1.0\n", False),
+        (H + "2 2 2\n1 1 1.0\n", False),
+        (H + "2 2 2\n1 1 2.0\n1 1 3.0\n", False),
+        (H + "2 2 2\n1 1 2.0\n1 1 3.0\n", True),
+        (H + "3 3 3\n1 1 +1.5\n2 2 1_000.25\n+3 0_3 -2e-3\n", False),
+        (H + "3 3 2\n1 1 1e999\n2 2 1e-999\n", False),
+        (H + "3 3 2\n1 1 inf\n2 2 -Infinity\n", False),
+        (H + "3 3 2\n1 1 1.0\n2 2 x\n", False),
+        (H + "3 3 1\n1 1 1.0\n2 2 3.0\n", False),
+        (H + "3 3 1\n1 1 1.0\n2 2\n", False),
+        (H + "3 3 1\n1 1 1.0\n2 2 zz\n", False),
+        (H + "3 3 2\n4 1 1.0\n1 1 zz\n", False),
+        (H + "3 3 2\n1 1 zz\n4 1 1.0\n", False),
+        (H + "3 3\n", False),
+        (H + "3 x 3\n", False),
+        (H + "% only comments\n", False),
+        ("%%MatrixMarket matrix coordinate complex general\n1 1 0\n", False),
+        ("%%matrixmarket matrix coordinate real general\n1 1 0\n", False),
+        ("", False),
+        (H + "2 2 0", False),
+        (H + "2 2 1", False),
+        (H + "  2   2   2  \n\n  1 1 1.0  \n\n 2 2   -0.0 \n", False),
+        (H + "4 5 3\n1 2 0.0\n3 4 2.0\n4 5 -1.0\n", False),
+        (H.replace("\n", "\r\n") + "2 2 1\r\n2 1 7.5\r\n", False),
+    ]
+    for _ in range(12):
+        r, c = int(rng.integers(1, 40)), int(rng.integers(1, 40))
+        n = int(rng.integers(0, r * c // 2 + 1))
+        A = ref_canon(r, c, rng.integers(0, r, n), rng.integers(0, c, n), rng.standard_normal(n) *
+                      10.0 ** rng.integers(-300, 300, n), "sum")
+        buf = _io.StringIO()
+        ref_io.save_mm(_mat(A, r, c), buf)
+        texts.append((buf.getvalue(), False))
+    vals = [1e-308, 1.0 / 3.0, float(np.nextafter(1.0, 2.0)), 1e300, -7.25, 5e-324]
+    buf = _io.StringIO()
+    ref_io.save_mm(SpMat.from_triplets(6, 1, [(i, 0, v) for i, v in enumerate(vals)]), buf)
+    texts.append((buf.getvalue(), False))
+    cases = []
+    for text, lenient in texts:
+        case = dict(text=np.frombuffer(text.encode("ascii"), np.uint8), lenient=int(lenient))
+        try:
+            m = ref_io.load_mm(text if "\n" in text else _io.StringIO(text), lenient_duplicates=lenient)
+            d = m.csc()
+            case.update(outcome="ok", n_rows=d.dims.n_rows, n_cols=d.dims.n_cols, out_vals=d.values,
+                        out_rows=d.row_indices, out_offs=d.col_offsets)
+            out = _io.StringIO()
+            ref_io.save_mm(m, out)
+            case["saved"] = np.frombuffer(out.getvalue().encode("ascii"), np.uint8)
+        except Exception as e:  # noqa: BLE001 -- the reference's exception is the expected outcome
+            case.update(outcome="error", err_class=type(e).__name__, err_msg=str(e))
+        cases.append(case)
+    save("mm", cases)
+
+
 def main(only=None):
     """No arguments: every file.  `funnel` alone: only funnel.npz (its own
     seed; the first seven share one generator stream in this order)."""
-    if not only or set(only) - {"funnel"}:
+    if not only or set(only) - {"funnel", "mm"}:
         rng = np.random.default_rng(20260809)
         gen_canonicalize(rng)
         gen_flush(rng)
@@ -322,6 +389,8 @@ def main(only=None):
         gen_trace(rng)
     if not only or "funnel" in only:
         gen_funnel(np.random.default_rng(20261019))
+    if not only or "mm" in only:
+        gen_mm(np.random.default_rng(20261020))
 
 
 if __name__ == "__main__":

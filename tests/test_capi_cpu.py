@@ -16,7 +16,7 @@ def _declared():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     out = {}
-    for m in re.finditer(r"\b(?:int|size_t|const char \*)\s*\*?\s*(as_\w+)\s*\(([^)]*)\)\s*;", src):
+    for m in re.finditer(r"\b(?:int|int64_t|size_t|const char \*)\s*\*?\s*(as_\w+)\s*\(([^)]*)\)\s*;", src):
         args = [a for a in m.group(2).split(",") if a.strip() and a.strip() != "void"]
         out[m.group(1)] = len(args)
     return out
