@@ -415,9 +415,16 @@ int64_t as_mm_format(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t*
         s.reserve((size_t)(hi - lo) * 32);
         char line[96];
         for (long long k = lo; k < hi; k++) {
-          const int n = snprintf(line, sizeof(line), "%lld %lld %.17g\n", (long long)rows[k] + 1,
-                                 (long long)cols[k] + 1, vals[k]);
-          s.append(line, (size_t)n);
+          // std::to_chars with a precision is specified to print exactly like
+          // printf("%.17g") (and is several times faster than snprintf)
+          char* q = line;
+          q = std::to_chars(q, line + sizeof(line), (long long)rows[k] + 1).ptr;
+          *q++ = ' ';
+          q = std::to_chars(q, line + sizeof(line), (long long)cols[k] + 1).ptr;
+          *q++ = ' ';
+          q = std::to_chars(q, line + sizeof(line), vals[k], std::chars_format::general, 17).ptr;
+          *q++ = '\n';
+          s.append(line, (size_t)(q - line));
         }
       });
     for (auto& x : th) x.join();
