@@ -281,3 +281,21 @@ def test_device_tensors_in_and_out():
     assert isinstance(C, torch.Tensor) and C.is_cuda
     want = m.to_dense() @ X.cpu().numpy()
     assert np.allclose(C.cpu().numpy(), want, rtol=0, atol=1e-12)
+
+
+def test_transposed_operand_reads_the_cached_csr():
+    """0.5*(A+B) @ C.t() -- the transpose is read through C's
+    cached CSR, not materialised; same result as the naive post-order."""
+    from paper_1805_03380_b200 import Add, Mul, ScalarMul, Transpose, evaluate_counting, lift
+
+    rng = np.random.default_rng(11)
+    mats = []
+    for _ in range(3):
+        d = np.where(rng.random((14, 14)) < 0.3, rng.standard_normal((14, 14)), 0.0)
+        mats.append(SpMat.from_dense(d, device="cuda"))
+    a, b, c = mats
+    e = Mul(ScalarMul(0.5, Add(lift(a), lift(b))), Transpose(lift(c)))
+    opt, t_opt = evaluate_counting(e, optimize=True)
+    naive, t_naive = evaluate_counting(e, optimize=False)
+    assert t_opt == 1 and t_naive == 3  # the scaled sum only / sum, scaling and transpose
+    assert opt.csc().same_elements(naive.csc())
