@@ -183,18 +183,19 @@ __global__ void __launch_bounds__(kMThreads) csc_add_kernel(AddArgs a) {
 }
 
 static int add_grid() {
-  static int grid = 0;
-  if (grid == 0) {
-    int per_sm = 0, dev = 0, sms = 0;
+  static int grid[kMaxDevices] = {0};  // per device: the attribute and occupancy are per device
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
+  if (grid[dev] == 0) {
+    int per_sm = 0, sms = 0;
     if (cudaFuncSetAttribute(csc_add_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(AddSmem)) !=
         cudaSuccess)
       return 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csc_add_kernel, kMThreads, sizeof(AddSmem));
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid = std::max(1, std::min(per_sm * sms, 148 * 8));
+    grid[dev] = std::max(1, std::min(per_sm * sms, 148 * 8));
   }
-  return grid;
+  return grid[dev];
 }
 
 }  // namespace as

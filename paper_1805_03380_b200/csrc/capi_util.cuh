@@ -52,6 +52,7 @@ struct Carve {
 };
 
 constexpr int kNumSMs = 148;
+constexpr int kMaxDevices = 64;  // per-device launch-configuration caches
 
 inline int grid_for(long long n, int block, int per_sm = 8) {
   long long g = (n + block - 1) / block;

@@ -92,18 +92,21 @@ static size_t carve_persist(Carve& c, PersistWs* w, long long n, long long n_col
 
 template <class T, class S1, class S2>
 static int launch_persist(PersistArgs<T, S1, S2>& a, cudaStream_t st) {
-  static int grid = 0;
+  static int grid_of[kMaxDevices] = {0};  // per device: the attribute and occupancy are per device
   const size_t smem = sizeof(PersistSmem<T>);
   auto kern = persist_bucket_kernel<T, S1, S2>;
-  if (grid == 0) {
+  int dev = 0;
+  AS_CUDA_TRY(cudaGetDevice(&dev));
+  AS_REQUIRE(dev >= 0 && dev < kMaxDevices, AS_ERR_CUDA, "device ordinal %d beyond %d", dev, kMaxDevices);
+  if (grid_of[dev] == 0) {
     AS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0, dev = 0, sms = 0;
+    int per_sm = 0, sms = 0;
     AS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSegThreads, smem));
-    AS_CUDA_TRY(cudaGetDevice(&dev));
     AS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     AS_REQUIRE(per_sm > 0, AS_ERR_CUDA, "persistent kernel does not fit on an SM");
-    grid = (int)std::min<long long>((long long)per_sm * sms, kMaxGrid);
+    grid_of[dev] = (int)std::min<long long>((long long)per_sm * sms, kMaxGrid);
   }
+  const int grid = grid_of[dev];
   void* args[] = {(void*)&a};
   AS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSegThreads), args, smem, st));
   return AS_OK;

@@ -245,16 +245,17 @@ trace_partial_kernel(long long n_cols, const int* __restrict__ ap, const int* __
 }
 
 static int trace_grid() {
-  static int grid = 0;
-  if (grid == 0) {
-    int per_sm = 0, dev = 0, sms = 0;
+  static int grid[kMaxDevices] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 148;
+  if (grid[dev] == 0) {
+    int per_sm = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_partial_kernel, kTrThreads, 0);
     per_sm = std::min(per_sm, 6);
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid = std::max(1, per_sm * sms);
+    grid[dev] = std::max(1, per_sm * sms);
   }
-  return grid;
+  return grid[dev];
 }
 
 }  // namespace as
