@@ -159,8 +159,13 @@ class CscData:
         return np.repeat(np.arange(self.dims.n_cols, dtype=np.int64), np.diff(self.col_offsets))
 
     def expand_cols_device(self) -> torch.Tensor:
-        counts = (self.col_ptr[1:] - self.col_ptr[:-1]).long()
-        return torch.repeat_interleave(torch.arange(self.dims.n_cols, device=self.device, dtype=torch.int32), counts)
+        """Column of every element (int32, on the device; as_expand_cols)."""
+        if self.device.type != "cuda":
+            counts = (self.col_ptr[1:] - self.col_ptr[:-1]).long()
+            return torch.repeat_interleave(torch.arange(self.dims.n_cols, dtype=torch.int32), counts)
+        from . import _kernels
+
+        return _kernels.expand_cols(self.dims.n_cols, self.col_ptr, self.nnz)
 
     def to_dense(self) -> np.ndarray:
         dense = np.zeros((self.dims.n_rows, self.dims.n_cols))
