@@ -251,6 +251,7 @@ struct PersistArgs {
   // taken in `order` (largest size class first)
   unsigned* cb_col;              // [n_cb + 1]
   unsigned* order;               // [n_cb] (pre_ptr mode only)
+  unsigned long long* tstate;    // [n_cb] zeroed: chained-scan states of the buckets' kept counts
 };
 
 // Variable-width buckets of pre-bucketed input: column c weighs
@@ -291,7 +292,7 @@ struct BTileSmem {
   unsigned ckept[kMaxW];  // kept per column (oversized path)
   unsigned obin[2 * kTBins + 1];  // bin starts of an oversized bucket's split
   unsigned long long cmin, cmax;  // (column, row) range of a tile
-  long long tile, s, m, col_base;
+  long long tile, s, m, col_base, prefix;
   int wt;
 };
 
@@ -598,7 +599,7 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int Wt, int row_bits) {
 // memory sort; a single bin still larger than the tile is radix-sorted in
 // global memory and streamed.  Values are read by input index.
 template <class T, class S1, class S2>
-__device__ void process_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a, long long s, long long m,
+__device__ long long process_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a, long long s, long long m,
                                          unsigned col_base, int Wt) {
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int W = Wt;
@@ -740,6 +741,7 @@ __device__ void process_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1, S2>
   }
   for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = S.ckept[l];
   __syncthreads();
+  return run_base;
 }
 
 template <class T, class S1, class S2>
@@ -754,11 +756,14 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
   const long long ncb = a.n_cb;
   const unsigned long long cb_mul = a.cb_mul;
   auto bucket_of = [&](unsigned c) -> unsigned { return (unsigned)(((unsigned long long)c * cb_mul) >> 32); };
+  // pre-bucketed SpGEMM products (NoSrc, NoSrc) vs construction / flush /
+  // transpose: separate instantiations, each without the other's code
+  constexpr bool kPre = std::is_same<S1, NoSrc<T>>::value && std::is_same<S2, NoSrc<T>>::value;
   AS_PHASE_MARK(a, 0);
   a.s1.set_cache(SM.h.colc);
   a.s2.set_cache(SM.h.colc);
 
-  if (a.pre_ptr != nullptr) {
+  if constexpr (kPre) {
     // pre-bucketed input (SpGEMM products): keys / colb / vals_b already sit
     // in output-column order; only the coarse bucket starts are needed
     // variable-width buckets (kPreT): bucket t starts at the first column whose
@@ -885,8 +890,31 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
     const long long s = S.s, m = S.m;
     const unsigned col_base = (unsigned)S.col_base;
     const int Wt = S.wt;  // columns of this bucket
+    // direct placement (construction / flush / transpose): the tickets hand
+    // the buckets out in order, so a chained look-back over their kept counts
+    // gives each bucket its output offset as soon as its own count is known
+    // -- no column-scan or placement phase, no temporaries (pre mode keeps
+    // them: its largest-first tile order would break the look-back chain)
+    auto lookback = [&](long long kept) -> long long {
+      if (tid < 32) {
+        const unsigned long long pre = tile_lookback_warp(a.tstate, t, (unsigned long long)kept);
+        if (tid == 0) S.prefix = (long long)pre;
+      }
+      __syncthreads();
+      const long long base = S.prefix;
+      if (t == ncb - 1 && tid == 0) {
+        a.col_ptr[a.n_cols] = (int)(base + kept);
+        a.info[0] = base + kept;
+      }
+      return base;
+    };
     if (m == 0) {
-      for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = 0u;
+      if constexpr (kPre) {
+        for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = 0u;
+      } else {
+        const long long base = lookback(0);
+        for (int l = tid; l < Wt; l += nthr) a.col_ptr[col_base + l] = (int)base;
+      }
     } else if (m <= kCap) {
       {  // all loads of this thread in flight before the first store
         unsigned long long kk[kItems];
@@ -912,18 +940,50 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
       __syncthreads();
       sort_bucket_smem(S, (int)m, Wt, a.row_bits);
       bucket_chunk_reduce<T>(S, 0, (int)m, m, nullptr, nullptr, col_base, a.vs, a.mode, a.prune, a.vals_b + s);
-      for (int p = tid; p < m; p += nthr) {
-        const unsigned e0 = S.v.excl[p], e1 = S.v.excl[p + 1];
-        if (e1 != e0) {
-          a.tmp_rows[s + e0] = (int)key_row(S.sk[p]);
-          a.tmp_vals[s + e0] = S.u.rv[p];
+      if constexpr (kPre) {
+        for (int p = tid; p < m; p += nthr) {
+          const unsigned e0 = S.v.excl[p], e1 = S.v.excl[p + 1];
+          if (e1 != e0) {
+            a.tmp_rows[s + e0] = (int)key_row(S.sk[p]);
+            a.tmp_vals[s + e0] = S.u.rv[p];
+          }
+        }
+        for (int l = tid; l < Wt; l += nthr)
+          a.col_kept[col_base + l] = S.v.excl[S.cstart[l + 1]] - S.v.excl[S.cstart[l]];
+      } else {
+        const long long base = lookback((long long)S.v.excl[m]);
+        for (int p = tid; p < m; p += nthr) {
+          const unsigned e0 = S.v.excl[p], e1 = S.v.excl[p + 1];
+          if (e1 != e0) {
+            a.row_idx[base + e0] = (int)key_row(S.sk[p]);
+            a.out_vals[base + e0] = S.u.rv[p];
+          }
+        }
+        for (int l = tid; l < Wt; l += nthr) a.col_ptr[col_base + l] = (int)(base + S.v.excl[S.cstart[l]]);
+      }
+    } else {
+      const long long kept = process_oversized_bucket<T>(S, a, s, m, col_base, Wt);
+      if constexpr (!kPre) {
+        const long long base = lookback(kept);
+        for (long long i = tid; i < kept; i += nthr) {
+          a.row_idx[base + i] = __ldcg(&a.tmp_rows[s + i]);
+          a.out_vals[base + i] = __ldcg(&a.tmp_vals[s + i]);
+        }
+        long long running = base;  // col_ptr of the bucket's columns: scan of the kept counts
+        for (int l0 = 0; l0 < Wt; l0 += nthr) {
+          const int l = l0 + tid;
+          long long tot;
+          const long long ex = block_exclusive_scan<long long>(l < Wt ? (long long)S.ckept[l] : 0ll, xscan, &tot);
+          if (l < Wt) a.col_ptr[col_base + l] = (int)(running + ex);
+          running += tot;
         }
       }
-      for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = S.v.excl[S.cstart[l + 1]] - S.v.excl[S.cstart[l]];
-    } else {
-      process_oversized_bucket<T>(S, a, s, m, col_base, Wt);
     }
     __syncthreads();
+  }
+  if constexpr (!kPre) {
+    AS_PHASE_MARK(a, gen + 1);
+    return;
   }
   grid_sync(a.gb, gen);
   AS_PHASE_MARK(a, gen);

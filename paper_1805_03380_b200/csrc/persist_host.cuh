@@ -29,6 +29,7 @@ struct PersistWs {
   long long* own_info;
   unsigned* cb_col;  // [n_cb + 1] first column of each bucket
   unsigned* order;   // pre-bucketed input only
+  unsigned long long* tstate;
   unsigned long long cb_mul;
   bool ok;           // the column count is supported
   long long n_cb;
@@ -72,6 +73,7 @@ static size_t carve_persist(Carve& c, PersistWs* w, long long n, long long n_col
   }
   w->zero = c.take<unsigned>(64);
   w->cb_cnt = c.take<unsigned>(std::max(1ll, w->n_cb));  // pre: size class and slot of each bucket
+  w->tstate = c.take<unsigned long long>(std::max(1ll, w->n_cb));
   w->zero_bytes = c.off;
   w->cb_start = c.take<long long>(w->n_cb + 1);
   w->cb_col = c.take<unsigned>(w->n_cb + 1);
@@ -157,6 +159,7 @@ static int run_persist_ws(PersistWs& w, const S1& s1, const S2& s2, long long n,
   a.pre_ptr = pre_ptr;
   a.cb_col = w.cb_col;
   a.order = pre_ptr ? w.order : nullptr;
+  a.tstate = w.tstate;
   static unsigned long long* dbg_ts = nullptr;
   const bool phase_dbg = getenv("AS_PHASE_TIMES") != nullptr;
   if (phase_dbg) {
