@@ -60,6 +60,42 @@ constexpr int kExItems = 8;
 constexpr int kExRange = kExThreads * kExItems;  // products per CTA
 constexpr int kExWin = kExRange + 1;             // staged B entries (longer windows search globally)
 
+// For every product range t: the first / last B entry it touches and their
+// columns (one thread per range; the expand CTAs then start without a
+// dependent chain of global binary searches).
+__global__ void __launch_bounds__(kExThreads)
+spgemm_range_bounds_kernel(long long n_ranges, long long nnz_b, long long n_cols_b, long long total,
+                           const int* __restrict__ b_ptr, const long long* __restrict__ ent_ptr,
+                           long long* __restrict__ bounds) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n_ranges;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long P0 = t * kExRange, P1 = min(total, P0 + kExRange);
+    auto last_le = [&](long long q) {  // last entry with ent_ptr <= q
+      long long lo = 0, hi = nnz_b - 1;
+      while (lo < hi) {
+        const long long mid = (lo + hi + 1) >> 1;
+        if (__ldg(&ent_ptr[mid]) <= q) lo = mid;
+        else hi = mid - 1;
+      }
+      return lo;
+    };
+    auto col_of = [&](long long kk) {  // last j with b_ptr[j] <= kk
+      long long lo = 0, hi = n_cols_b - 1;
+      while (lo < hi) {
+        const long long mid = (lo + hi + 1) >> 1;
+        if (__ldg(&b_ptr[mid]) <= kk) lo = mid;
+        else hi = mid - 1;
+      }
+      return lo;
+    };
+    const long long kk0 = last_le(P0), kk1 = last_le(P1 - 1);
+    bounds[4 * t] = kk0;
+    bounds[4 * t + 1] = kk1;
+    bounds[4 * t + 2] = col_of(kk0);
+    bounds[4 * t + 3] = col_of(kk1);
+  }
+}
+
 // Flatten products [t*kExRange, (t+1)*kExRange) in reference order (entry kk
 // ascending, A position ascending): product q belongs to the last entry with
 // ent_ptr[kk] <= q.
@@ -68,44 +104,18 @@ spgemm_expand_kernel(long long nnz_b, long long n_cols_b, long long total, const
                      const int* __restrict__ a_rows, const double* __restrict__ a_vals,
                      const int* __restrict__ b_ptr, const int* __restrict__ b_rows,
                      const double* __restrict__ b_vals, const long long* __restrict__ ent_ptr,
-                     unsigned long long* __restrict__ keys, unsigned* __restrict__ colb, double* __restrict__ pvals) {
+                     const long long* __restrict__ bounds, unsigned long long* __restrict__ keys,
+                     unsigned* __restrict__ colb, double* __restrict__ pvals) {
   __shared__ int s_off[kExWin];  // ent_ptr[kk] - P0 (clamped below at 0 for the first entry)
   __shared__ int s_ast[kExWin];  // A column start of the entry, shifted to the entry's product 0
   __shared__ int s_col[kExWin];
   __shared__ double s_bv[kExWin];
-  __shared__ long long s_kk0, s_kk1, s_j0, s_j1;
   const int tid = threadIdx.x;
   for (long long t = blockIdx.x; t * kExRange < total; t += gridDim.x) {
     const long long P0 = t * kExRange, P1 = min(total, P0 + kExRange);
     __syncthreads();
-    if (tid == 0) {
-      // last entry with ent_ptr <= P0, and with ent_ptr <= P1 - 1
-      auto last_le = [&](long long q) {
-        long long lo = 0, hi = nnz_b - 1;
-        while (lo < hi) {
-          const long long mid = (lo + hi + 1) >> 1;
-          if (__ldg(&ent_ptr[mid]) <= q) lo = mid;
-          else hi = mid - 1;
-        }
-        return lo;
-      };
-      const long long kk0 = last_le(P0), kk1 = last_le(P1 - 1);
-      auto col_of = [&](long long kk) {  // last j with b_ptr[j] <= kk
-        long long lo = 0, hi = n_cols_b - 1;
-        while (lo < hi) {
-          const long long mid = (lo + hi + 1) >> 1;
-          if (__ldg(&b_ptr[mid]) <= kk) lo = mid;
-          else hi = mid - 1;
-        }
-        return lo;
-      };
-      s_kk0 = kk0;
-      s_kk1 = kk1;
-      s_j0 = col_of(kk0);
-      s_j1 = col_of(kk1);
-    }
-    __syncthreads();
-    const long long kk0 = s_kk0, kk1 = s_kk1, j0 = s_j0, j1 = s_j1;
+    const long long kk0 = __ldg(&bounds[4 * t]), kk1 = __ldg(&bounds[4 * t + 1]);
+    const long long j0 = __ldg(&bounds[4 * t + 2]), j1 = __ldg(&bounds[4 * t + 3]);
     const int nw = (int)(kk1 - kk0 + 1);
     const bool staged = nw <= kExWin;
     if (staged) {
@@ -210,7 +220,7 @@ int as_spgemm_products(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, cons
 
 static void carve_spgemm(Carve& c, PersistWs* w, long long n_cols_b, long long nnz_b, long long total,
                          unsigned** scan_zero, size_t* scan_zero_bytes, unsigned long long** states, unsigned** lens,
-                         long long** ent_ptr) {
+                         long long** ent_ptr, long long** bounds) {
   carve_persist(c, w, total, n_cols_b, sizeof(double), true);
   const long long per = (long long)kScanThreads * kScanItems;
   const long long tiles = nnz_b > 0 ? (nnz_b + per - 1) / per : 1;
@@ -220,6 +230,7 @@ static void carve_spgemm(Carve& c, PersistWs* w, long long n_cols_b, long long n
   *scan_zero_bytes = c.off - z0;
   *lens = c.take<unsigned>(std::max(1ll, nnz_b));
   *ent_ptr = c.take<long long>(nnz_b + 1);
+  *bounds = c.take<long long>(4 * std::max(1ll, (total + kExRange - 1) / kExRange));
 }
 
 size_t as_spgemm_workspace_bytes(int64_t n_cols_b, int64_t nnz_b, int64_t total_products) {
@@ -228,8 +239,8 @@ size_t as_spgemm_workspace_bytes(int64_t n_cols_b, int64_t nnz_b, int64_t total_
   unsigned *z, *lens;
   size_t zb;
   unsigned long long* states;
-  long long* ent;
-  carve_spgemm(c, &w, n_cols_b, nnz_b, total_products, &z, &zb, &states, &lens, &ent);
+  long long *ent, *bounds;
+  carve_spgemm(c, &w, n_cols_b, nnz_b, total_products, &z, &zb, &states, &lens, &ent, &bounds);
   return c.off;
 }
 
@@ -248,8 +259,8 @@ int as_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int
   unsigned *scan_zero, *lens;
   size_t zb;
   unsigned long long* states;
-  long long* ent_ptr;
-  carve_spgemm(c, &w, n_cols_b, nnz_b, total_products, &scan_zero, &zb, &states, &lens, &ent_ptr);
+  long long *ent_ptr, *bounds;
+  carve_spgemm(c, &w, n_cols_b, nnz_b, total_products, &scan_zero, &zb, &states, &lens, &ent_ptr, &bounds);
   AS_REQUIRE(c.ok, AS_ERR_ARG, "workspace too small: %zu < %zu", ws_bytes, c.off);
   if (n_cols_b > 0 && nnz_b > 0 && total_products > 0) {
     const long long per = (long long)kScanThreads * kScanItems;
@@ -260,9 +271,12 @@ int as_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int
     count_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(lens, nnz_b, ent_ptr, states, scan_zero);
     AS_LAUNCH_CHECK();
     const long long ranges = (total_products + kExRange - 1) / kExRange;
+    spgemm_range_bounds_kernel<<<grid_for(ranges, kExThreads), kExThreads, 0, st>>>(
+        ranges, nnz_b, n_cols_b, total_products, b_col_ptr, ent_ptr, bounds);
+    AS_LAUNCH_CHECK();
     spgemm_expand_kernel<<<(unsigned)std::min<long long>(ranges, (long long)kNumSMs * 32), kExThreads, 0, st>>>(
-        nnz_b, n_cols_b, total_products, a_col_ptr, a_row_idx, a_vals, b_col_ptr, b_row_idx, b_vals, ent_ptr, w.keys,
-        w.colb, (double*)w.vals_b);
+        nnz_b, n_cols_b, total_products, a_col_ptr, a_row_idx, a_vals, b_col_ptr, b_row_idx, b_vals, ent_ptr, bounds,
+        w.keys, w.colb, (double*)w.vals_b);
     AS_LAUNCH_CHECK();
   }
   ValSrc<double> vs{(const double*)w.vals_b, nullptr, (unsigned long long)total_products};
