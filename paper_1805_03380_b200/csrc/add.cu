@@ -93,6 +93,7 @@ struct AddArgs {
   double* out_vals;
   long long* info;
   long long* cta_sums;
+  unsigned char* tcount;  // [n_chunks * kMThreads] pass-1 output count of every thread's positions
   GridBar gb;
 };
 
@@ -133,6 +134,7 @@ __global__ void __launch_bounds__(kMThreads) csc_add_kernel(AddArgs a) {
     if (d0 < d1)
       merge_range(a.n_cols, col_of(S.W, a.ap, a.bp, a.n_cols, d0), d0, d1, a.ap, a.ar, a.av, a.bp, a.br, a.bv, a.alpha,
                   a.beta, [&](int, double) { cnt++; }, no_col);
+    a.tcount[(chunk / kAddChunk) * kMThreads + tid] = (unsigned char)cnt;  // reused by pass 2
     total += block_reduce_sum<long long>((long long)cnt, S.scan_tmp);
   }
   if (tid == 0) a.cta_sums[blockIdx.x] = total;
@@ -148,10 +150,7 @@ __global__ void __launch_bounds__(kMThreads) csc_add_kernel(AddArgs a) {
     const long long d0 = chunk + (long long)tid * kAddItems;
     const long long d1 = min(d0 + kAddItems, min(hi, chunk + kAddChunk));
     const long long c0 = d0 < d1 ? col_of(S.W, a.ap, a.bp, a.n_cols, d0) : 0;
-    int cnt = 0;
-    if (d0 < d1)
-      merge_range(a.n_cols, c0, d0, d1, a.ap, a.ar, a.av, a.bp, a.br, a.bv, a.alpha, a.beta,
-                  [&](int, double) { cnt++; }, no_col);
+    const int cnt = __ldcg(&a.tcount[(chunk / kAddChunk) * kMThreads + tid]);
     long long ctot;
     const long long off = block_exclusive_scan<long long>((long long)cnt, S.scan_tmp, &ctot);
     int w = (int)off;
@@ -206,9 +205,8 @@ extern "C" {
 
 size_t as_add_workspace_bytes(int64_t n_cols, int64_t nnz_a, int64_t nnz_b) {
   (void)n_cols;
-  (void)nnz_a;
-  (void)nnz_b;
-  return 256 + (size_t)148 * 8 * sizeof(long long);
+  const long long n_chunks = (nnz_a + nnz_b + kAddChunk - 1) / kAddChunk;
+  return 256 + (size_t)148 * 8 * sizeof(long long) + (size_t)(n_chunks + 1) * kMThreads;
 }
 
 int as_csc_add_f64(int64_t n_rows, int64_t n_cols, double alpha, double beta, const int32_t* a_col_ptr,
@@ -237,6 +235,7 @@ int as_csc_add_f64(int64_t n_rows, int64_t n_cols, double alpha, double beta, co
   a.out_vals = out_vals;
   a.info = (long long*)info;
   a.cta_sums = (long long*)((char*)ws + 256);
+  a.tcount = (unsigned char*)(a.cta_sums + 148 * 8);
   a.gb = GridBar{(unsigned*)ws, (unsigned*)ws + 32};
   void* args[] = {(void*)&a};
   AS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)csc_add_kernel, dim3(grid), dim3(kMThreads), args,
