@@ -314,6 +314,8 @@ def main_device(args):
     e2e_value = world * n * args.steps / e2e_total
     e2e = {"value": e2e_value, "unit": "nnz/s", "h2d_bytes_per_step": 24 * n,
            "d2h_bytes_per_step": 4 * (n_cols + 1) + 12 * k,
+           "ms_median": 1e3 * statistics.median(e2e_times), "ms_min": 1e3 * min(e2e_times),
+           "ms_max": 1e3 * max(e2e_times),
            "path": "SpMat.from_triplets((rows i64, cols i64, vals f64) pinned host) -> CSC read back to pinned host"}
 
     # ------------------------------------------------------------ other hot-path ops (rank 0)
