@@ -188,7 +188,10 @@ spmm_rows_lanes_kernel(long long n_rows, const int* __restrict__ row_ptr, const 
   const int beg = __ldg(&row_ptr[r]), end = __ldg(&row_ptr[r + 1]);
   // batches of kB entries: all indices, then all gathers (predicated), then
   // the folds in entry order -- two dependent round trips per batch
-  constexpr int kB = 8;
+#ifndef AS_SPMM_KB
+#define AS_SPMM_KB 8
+#endif
+  constexpr int kB = AS_SPMM_KB;
   for (int k = beg; k < end; k += kB) {
     int j[kB];
     T v[kB];
