@@ -32,21 +32,29 @@ def _read_info(info):
     return nnz, bad
 
 
-def coo_to_csc(n_rows, n_cols, rows, cols, vals, dup=DUP_SUM):
+def coo_to_csc(n_rows, n_cols, rows, cols, vals, dup=DUP_SUM, out=None):
     """Canonical CSC from COO triplets (csc.canonicalize, csc.py:148-193):
     stable column-major order, duplicates summed in np.add.reduceat order or
-    last-wins, exact zeros pruned.  rows/cols int32 or int64 on the device.
-    Returns (col_ptr, row_idx, vals, first_bad) where first_bad is the index
-    of the first out-of-range triplet or None (those are skipped)."""
+    last-wins, exact zeros pruned.  rows/cols int32 or int64, on the device or
+    in pinned host memory (then read over PCIe inside the kernel); `out` =
+    (col_ptr, row_idx, vals) buffers to write (device or pinned host, sized
+    n_cols + 1 / n / n).  Returns (col_ptr, row_idx, vals, first_bad) where
+    first_bad is the index of the first out-of-range triplet or None (those
+    are skipped)."""
     L = _lib.lib()
-    dev = vals.device
+    dev = vals.device if vals.is_cuda else torch.device("cuda", torch.cuda.current_device())
     n = int(vals.shape[0])
     assert rows.dtype == cols.dtype and rows.dtype in (torch.int32, torch.int64)
+    if not vals.is_cuda and n > 0:
+        assert rows.is_pinned() and cols.is_pinned() and vals.is_pinned(), "host triplets must be pinned"
     idx_bytes = 4 if rows.dtype == torch.int32 else 8
     f = L.as_coo_to_csc_f64 if vals.dtype == torch.float64 else L.as_coo_to_csc_f32
-    col_ptr = torch.empty(n_cols + 1, dtype=torch.int32, device=dev)
-    row_idx = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    out_vals = torch.empty(max(n, 1), dtype=vals.dtype, device=dev)
+    if out is not None:
+        col_ptr, row_idx, out_vals = out
+    else:
+        col_ptr = torch.empty(n_cols + 1, dtype=torch.int32, device=dev)
+        row_idx = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        out_vals = torch.empty(max(n, 1), dtype=vals.dtype, device=dev)
     info = torch.empty(2, dtype=torch.int64, device=dev)
     ws_bytes = L.as_build_workspace_bytes(n, n_cols)
     ws = workspace(ws_bytes, dev)

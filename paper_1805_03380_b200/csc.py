@@ -242,6 +242,36 @@ def canonicalize(dims: Dims, rows, cols, values, dup: str = DUP_SUM, device=None
     return m
 
 
+def canonicalize_host(dims: Dims, rows, cols, values, dup: str = DUP_SUM, out=None) -> CscData:
+    """csc.canonicalize with host arrays in and out (the reference's own
+    numpy-in / numpy-out signature, csc.py:148-193): pinned host triplets are
+    read over PCIe by the build kernel itself and the CSC is written straight
+    into pinned host memory (`out` = (col_ptr int32[n_cols+1], row_idx
+    int32[n], vals float64[n]) to reuse), so both transfers overlap the
+    kernel's own phases.  Returns a host CscData."""
+    if dup not in (DUP_SUM, DUP_LAST):
+        raise ValueError("unknown duplicate policy %r" % (dup,))
+
+    def pinned(a, dtype):
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+        if t.dtype != dtype:
+            t = t.to(dtype)
+        return t if t.is_pinned() else t.pin_memory()
+
+    idx_t = torch.int64
+    r, c = pinned(rows, idx_t), pinned(cols, idx_t)
+    v = pinned(values, torch.float64)
+    n = int(v.shape[0])
+    if out is None:
+        out = (torch.empty(dims.n_cols + 1, dtype=torch.int32).pin_memory(),
+               torch.empty(max(n, 1), dtype=torch.int32).pin_memory(),
+               torch.empty(max(n, 1), dtype=torch.float64).pin_memory())
+    p, ri, vv, bad = _kernels.coo_to_csc(dims.n_rows, dims.n_cols, r, c, v, dup, out=out)
+    if bad is not None:
+        raise CoordinateError("coordinate %d outside %s matrix" % (bad, dims))
+    return CscData(dims, p, ri, vv, device=torch.device("cpu"))
+
+
 def _coords_from_triplets(triplets: Sequence) -> tuple:
     """(rows, cols, values) from a reference-style triplet sequence
     (csc.py:196-205), or passed through when given as three arrays."""

@@ -16,6 +16,24 @@
 
 namespace as {
 
+// pinned (or mapped) host memory: device-accessible through UVA
+static bool is_host_pointer(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+inline size_t staging_bytes(long long n, size_t val_bytes) {
+  Carve c(nullptr, 0);
+  c.take<int>(n);
+  c.take<int>(n);
+  c.take<char>(n * (long long)val_bytes);
+  return c.off;
+}
+
 template <class T, class IdxT>
 static int coo_to_csc(long long n_rows, long long n_cols, long long n, const IdxT* rows, const IdxT* cols,
                       const T* vals, int dup, int* col_ptr, int* row_idx, T* out_vals, long long* info, void* ws,
@@ -25,9 +43,24 @@ static int coo_to_csc(long long n_rows, long long n_cols, long long n, const Idx
   AS_REQUIRE(n >= 0 && n <= kMaxDim, AS_ERR_ARG, "triplet count %lld outside the int32 range", n);
   AS_REQUIRE(dup == AS_DUP_SUM || dup == AS_DUP_LAST, AS_ERR_ARG, "unknown duplicate policy %d", dup);
   CooSrc<IdxT, T> s1{rows, cols, vals, n, n_rows, n_cols, 0ull, info + 1};
+  const int mode = dup == AS_DUP_SUM ? kSumPairwise : kLast;
+  const int row_bits = bits_for(n_rows > 0 ? n_rows - 1 : 0);
+  if (n > 0 && is_host_pointer(rows)) {
+    // pinned host triplets: read once over PCIe inside the kernel (CooHostSrc),
+    // staged in the tail of the workspace; outputs may be pinned host memory too
+    AS_REQUIRE(is_host_pointer(cols) && is_host_pointer(vals), AS_ERR_ARG,
+               "rows, cols and vals must all be device or all pinned host memory");
+    const size_t pb = persist_ws_bytes(n, n_cols, sizeof(T));
+    AS_REQUIRE(ws_bytes >= pb + staging_bytes(n, sizeof(T)), AS_ERR_ARG, "workspace too small for host input");
+    Carve c((char*)ws + pb, ws_bytes - pb);
+    CooHostSrc<IdxT, T> hs{s1, c.take<int>(n), c.take<int>(n), c.take<T>(n)};
+    AS_CUDA_TRY(cudaMemsetAsync(hs.st_rows, 0xff, (size_t)n * sizeof(int), st));  // skipped bad triplets stay -1
+    ValSrc<T> vs{hs.st_vals, nullptr, (unsigned long long)n};
+    return run_persist<T>(hs, NoSrc<T>{}, n_cols, row_bits, mode, 1, vs, col_ptr, row_idx, out_vals, info, true, ws,
+                          pb, st);
+  }
   ValSrc<T> vs{vals, nullptr, (unsigned long long)n};
-  return run_persist<T>(s1, NoSrc<T>{}, n_cols, bits_for(n_rows > 0 ? n_rows - 1 : 0),
-                        dup == AS_DUP_SUM ? kSumPairwise : kLast, 1, vs, col_ptr, row_idx, out_vals, info, true, ws,
+  return run_persist<T>(s1, NoSrc<T>{}, n_cols, row_bits, mode, 1, vs, col_ptr, row_idx, out_vals, info, true, ws,
                         ws_bytes, st);
 }
 
@@ -50,7 +83,10 @@ using namespace as;
 
 extern "C" {
 
-size_t as_build_workspace_bytes(int64_t n, int64_t n_cols) { return persist_ws_bytes(n, n_cols, 8); }
+// (includes the staging of pinned-host triplets; a device-input build uses only the first part)
+size_t as_build_workspace_bytes(int64_t n, int64_t n_cols) {
+  return persist_ws_bytes(n, n_cols, 8) + staging_bytes(n, 8);
+}
 size_t as_flush_workspace_bytes(int64_t nnz_base, int64_t n_log, int64_t n_cols) {
   return persist_ws_bytes(nnz_base + n_log, n_cols, 8);
 }

@@ -134,6 +134,38 @@ struct CooSrc {
   AS_DEVICE_INLINE void set_cache(int*) {}
 };
 
+// COO triplets in pinned HOST memory (zero-copy over PCIe).  The first pass
+// (phase 1, report = true) streams them once from the host -- coalesced, so
+// the transfer runs at PCIe speed while the histogram is built -- and stages
+// int32 rows / cols and the values in device memory; the second pass (phase
+// 3) reads the staged copy.  The host->device copy thus happens inside the
+// kernel, overlapped with its first phase (as_coo_to_csc_f64 on host pointers).
+template <class IdxT, class T>
+struct CooHostSrc {
+  CooSrc<IdxT, T> host;  // the triplets as given (host pointers, valid on the device through UVA)
+  int* st_rows;
+  int* st_cols;
+  T* st_vals;
+
+  template <bool kVal = false, class F>
+  __device__ void visit(long long p, long long P, bool report, F f) const {
+    if (report) {
+      host.template visit<true>(p, P, true, [&](unsigned c, unsigned r, unsigned long long idx, long long e, T v) {
+        st_rows[e] = (int)r;
+        st_cols[e] = (int)c;
+        st_vals[e] = v;
+        f(c, r, idx, e, v);
+      });
+    } else {
+      CooSrc<int, T> dev{st_rows, st_cols, st_vals, host.n, host.n_rows, host.n_cols, host.idx_off, nullptr};
+      dev.template visit<kVal>(p, P, false, f);
+    }
+  }
+  AS_DEVICE_INLINE T value(long long i) const { return st_vals[i]; }
+  __host__ __device__ long long size() const { return host.n; }
+  AS_DEVICE_INLINE void set_cache(int*) {}
+};
+
 // The elements of a CSC: by_row = false -> output column = col, minor = row
 // (flush base); by_row = true -> output column = row, minor = col (transpose).
 // Chunk p is the element range [p*ch, (p+1)*ch); the column starts it spans

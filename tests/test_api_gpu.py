@@ -299,3 +299,33 @@ def test_transposed_operand_reads_the_cached_csr():
     naive, t_naive = evaluate_counting(e, optimize=False)
     assert t_opt == 1 and t_naive == 3  # the scaled sum only / sum, scaling and transpose
     assert opt.csc().same_elements(naive.csc())
+
+
+def test_canonicalize_host_zero_copy():
+    """csc.canonicalize_host: pinned host triplets read over PCIe inside the
+    build kernel, the CSC written straight into pinned host memory; same
+    result as the device path and the oracle, bad triplets reported."""
+    import torch
+
+    import oracle
+    from paper_1805_03380_b200 import csc as C
+    from paper_1805_03380_b200.csc import Dims
+    from paper_1805_03380_b200.errors import CoordinateError
+
+    rng = np.random.default_rng(21)
+    for (r, c, n) in [(300, 200, 5000), (7, 5, 300), (10000, 10000, 200000), (50, 40, 0)]:
+        rows, cols, vals = rng.integers(0, r, n), rng.integers(0, c, n), rng.uniform(-1, 1, n)
+        got = C.canonicalize_host(Dims(r, c), rows, cols, vals)
+        assert got.col_ptr.device.type == "cpu"
+        want = oracle.canonicalize(r, c, rows, cols, vals)
+        assert np.array_equal(got.col_offsets, want[2]) and np.array_equal(got.row_indices, want[1])
+        assert np.array_equal(got.values.view(np.int64), want[0].view(np.int64))
+    rows = np.array([0, 5, 1], dtype=np.int64)
+    with pytest.raises(CoordinateError, match="coordinate 1"):
+        C.canonicalize_host(Dims(3, 3), rows, np.array([0, 0, 1]), np.array([1.0, 2.0, 3.0]))
+    # reused pinned output buffers, LastWins
+    out = (torch.empty(4, dtype=torch.int32).pin_memory(), torch.empty(4, dtype=torch.int32).pin_memory(),
+           torch.empty(4, dtype=torch.float64).pin_memory())
+    m = C.canonicalize_host(Dims(2, 3), np.array([1, 1, 0, 1]), np.array([0, 0, 2, 0]),
+                            np.array([2.0, 3.0, 9.0, 4.0]), C.DUP_LAST, out=out)
+    assert m.get(1, 0) == 4.0 and m.get(0, 2) == 9.0 and m.nnz == 2
