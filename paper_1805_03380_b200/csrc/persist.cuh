@@ -284,6 +284,12 @@ struct PersistArgs {
   unsigned* cb_col;              // [n_cb + 1]
   unsigned* order;               // [n_cb] (pre_ptr mode only)
   unsigned long long* tstate;    // [n_cb] zeroed: chained-scan states of the buckets' kept counts
+  // two-level scatter (large inputs): super-buckets of sb_f consecutive buckets
+  int sb_f;                      // buckets per super-bucket (<= 1: single level)
+  long long n_sb;
+  unsigned* sb_cnt;              // [n_sb] zeroed: per-super-bucket range reservation
+  unsigned* sb_fill;             // [n_cb] zeroed: per-bucket fill of the second scatter
+  T* vals_alt;                   // [n] staging of the first scatter
 };
 
 // Variable-width buckets of pre-bucketed input: column c weighs
@@ -776,7 +782,7 @@ __device__ long long process_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1
   return run_base;
 }
 
-template <class T, class S1, class S2>
+template <class T, class S1, class S2, bool kTwo = false>
 __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistArgs<T, S1, S2> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PersistSmem<T>& SM = *reinterpret_cast<PersistSmem<T>*>(smem_raw);
@@ -858,10 +864,29 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
     a.s2.visit(g, G, true, inc);
   }
   __syncthreads();
-  for (long long b = tid; b < ncb; b += nthr) {
-    const unsigned h = SM.h.a[b];
-    SM.h.b[b] = h ? atomicAdd(&a.cb_cnt[b], h) : 0u;
-    SM.h.a[b] = 0u;
+  const int F = a.sb_f;
+  const long long nsb = a.n_sb;
+  if constexpr (kTwo) {
+    // two-level: this CTA reserves its range inside every super-bucket (runs of
+    // >= ~32 elements per CTA, so the first scatter writes whole sectors) and
+    // adds its per-bucket counts to the global bucket totals
+    for (long long sb = tid; sb < nsb; sb += nthr) {
+      unsigned sum = 0;
+      for (long long b = sb * F; b < min(ncb, sb * F + F); b++) sum += SM.h.a[b];
+      SM.h.b[sb] = sum ? atomicAdd(&a.sb_cnt[sb], sum) : 0u;
+    }
+    for (long long b = tid; b < ncb; b += nthr) {
+      const unsigned h = SM.h.a[b];
+      if (h) atomicAdd(&a.cb_cnt[b], h);
+    }
+    __syncthreads();
+    for (long long b = tid; b < ncb; b += nthr) SM.h.a[b] = 0u;  // super-bucket cursors
+  } else {
+    for (long long b = tid; b < ncb; b += nthr) {
+      const unsigned h = SM.h.a[b];
+      SM.h.b[b] = h ? atomicAdd(&a.cb_cnt[b], h) : 0u;
+      SM.h.a[b] = 0u;
+    }
   }
   grid_sync(a.gb, gen);
   AS_PHASE_MARK(a, gen);
@@ -875,7 +900,11 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
       long long ctot;
       const long long ex = block_exclusive_scan<long long>(cnt, xscan, &ctot);
       if (b < ncb) {
-        SM.h.b[b] += (unsigned)(running + ex);  // slot base of this CTA's range
+        if constexpr (kTwo) {
+          if (b % F == 0) SM.h.b[b / F] += (unsigned)(running + ex);  // super-bucket start
+        } else {
+          SM.h.b[b] += (unsigned)(running + ex);  // slot base of this CTA's range
+        }
         if (g == 0) a.cb_start[b] = running + ex;
       }
       running += ctot;
@@ -885,20 +914,101 @@ __global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistA
   __syncthreads();
 
   // ---------------- phase 3: scatter keys, columns and values ----------------
-  a.s1.template visit<true>(g, G, false, [&](unsigned c, unsigned minor, unsigned long long idx, long long, T v) {
-    const unsigned cb = bucket_of(c);
-    const unsigned slot = SM.h.b[cb] + atomicAdd(&SM.h.a[cb], 1u);
-    a.keys[slot] = ((unsigned long long)minor << 32) | idx;
-    a.colb[slot] = c;
-    a.vals_b[slot] = v;
-  });
-  a.s2.template visit<true>(g, G, false, [&](unsigned c, unsigned minor, unsigned long long idx, long long, T v) {
-    const unsigned cb = bucket_of(c);
-    const unsigned slot = SM.h.b[cb] + atomicAdd(&SM.h.a[cb], 1u);
-    a.keys[slot] = ((unsigned long long)minor << 32) | idx;
-    a.colb[slot] = c;
-    a.vals_b[slot] = v;
-  });
+  if constexpr (kTwo) {
+    // 3a: into super-bucket order (alt arrays)
+    auto put = [&](unsigned c, unsigned minor, unsigned long long idx, long long, T v) {
+      const unsigned sb = bucket_of(c) / (unsigned)F;
+      const unsigned slot = SM.h.b[sb] + atomicAdd(&SM.h.a[sb], 1u);
+      a.keys_alt[slot] = ((unsigned long long)minor << 32) | idx;
+      a.colb_alt[slot] = c;
+      a.vals_alt[slot] = v;
+    };
+    a.s1.template visit<true>(g, G, false, put);
+    a.s2.template visit<true>(g, G, false, put);
+    grid_sync(a.gb, gen);
+    AS_PHASE_MARK(a, gen);
+    // 3b: fixed slices of the super-bucket-ordered data, each spread over its
+    // (<= 2F) buckets: count, reserve one range per bucket (global fill
+    // counters), scatter -- runs of ~slice/F elements, whole sectors again
+    constexpr long long kSlice = 8192;
+    const long long n_all = __ldcg(&a.cb_start[ncb]);
+    const long long n_slices = (n_all + kSlice - 1) / kSlice;
+    for (long long t = g; t < n_slices; t += G) {
+      const long long lo = t * kSlice, hi = min(n_all, lo + kSlice);
+      __syncthreads();
+      if (tid == 0) {  // first bucket of the super-bucket holding `lo`
+        long long l = 0, h = nsb - 1;
+        while (l < h) {
+          const long long mid = (l + h + 1) >> 1;
+          if (__ldcg(&a.cb_start[mid * F]) <= lo) l = mid;
+          else h = mid - 1;
+        }
+        S.tile = l * F;
+      }
+      __syncthreads();
+      const long long bb = S.tile;
+      const long long nbk = min(ncb - bb, 2ll * F);
+      for (long long f = tid; f < nbk; f += nthr) SM.h.a[f] = 0u;
+      __syncthreads();
+      constexpr int kU = 8;  // loads of kU elements in flight per thread
+      for (long long i0 = lo + tid; i0 < hi; i0 += (long long)kU * nthr) {
+        unsigned cc[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+          const long long i = i0 + (long long)u * nthr;
+          cc[u] = i < hi ? __ldcg(&a.colb_alt[i]) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; u++)
+          if (i0 + (long long)u * nthr < hi) atomicAdd(&SM.h.a[bucket_of(cc[u]) - bb], 1u);
+      }
+      __syncthreads();
+      for (long long f = tid; f < nbk; f += nthr) {
+        const unsigned h = SM.h.a[f];
+        SM.h.b[f] = h ? (unsigned)__ldcg(&a.cb_start[bb + f]) + atomicAdd(&a.sb_fill[bb + f], h) : 0u;
+        SM.h.a[f] = 0u;
+      }
+      __syncthreads();
+      for (long long i0 = lo + tid; i0 < hi; i0 += (long long)kU * nthr) {
+        unsigned cc[kU];
+        unsigned long long kk[kU];
+        T vv[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+          const long long i = i0 + (long long)u * nthr;
+          if (i < hi) {
+            cc[u] = __ldcg(&a.colb_alt[i]);
+            kk[u] = __ldcg(&a.keys_alt[i]);
+            vv[u] = __ldcg(&a.vals_alt[i]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+          if (i0 + (long long)u * nthr >= hi) continue;
+          const unsigned f = bucket_of(cc[u]) - (unsigned)bb;
+          const unsigned slot = SM.h.b[f] + atomicAdd(&SM.h.a[f], 1u);
+          a.keys[slot] = kk[u];
+          a.colb[slot] = cc[u];
+          a.vals_b[slot] = vv[u];
+        }
+      }
+    }
+  } else {
+    a.s1.template visit<true>(g, G, false, [&](unsigned c, unsigned minor, unsigned long long idx, long long, T v) {
+      const unsigned cb = bucket_of(c);
+      const unsigned slot = SM.h.b[cb] + atomicAdd(&SM.h.a[cb], 1u);
+      a.keys[slot] = ((unsigned long long)minor << 32) | idx;
+      a.colb[slot] = c;
+      a.vals_b[slot] = v;
+    });
+    a.s2.template visit<true>(g, G, false, [&](unsigned c, unsigned minor, unsigned long long idx, long long, T v) {
+      const unsigned cb = bucket_of(c);
+      const unsigned slot = SM.h.b[cb] + atomicAdd(&SM.h.a[cb], 1u);
+      a.keys[slot] = ((unsigned long long)minor << 32) | idx;
+      a.colb[slot] = c;
+      a.vals_b[slot] = v;
+    });
+  }
   grid_sync(a.gb, gen);
   AS_PHASE_MARK(a, gen);
   }

@@ -30,6 +30,11 @@ struct PersistWs {
   unsigned* cb_col;  // [n_cb + 1] first column of each bucket
   unsigned* order;   // pre-bucketed input only
   unsigned long long* tstate;
+  int sb_f;          // two-level scatter (sb_f > 1)
+  long long n_sb;
+  unsigned* sb_cnt;
+  unsigned* sb_fill;
+  void* vals_alt;
   unsigned long long cb_mul;
   bool ok;           // the column count is supported
   long long n_cb;
@@ -74,6 +79,19 @@ static size_t carve_persist(Carve& c, PersistWs* w, long long n, long long n_col
   w->zero = c.take<unsigned>(64);
   w->cb_cnt = c.take<unsigned>(std::max(1ll, w->n_cb));  // pre: size class and slot of each bucket
   w->tstate = c.take<unsigned long long>(std::max(1ll, w->n_cb));
+  // two-level scatter when the scattered element data outgrows L2 and a
+  // (CTA, bucket) run would be short: super-buckets of sb_f buckets so a
+  // (CTA, super-bucket) run averages >= 32 elements
+  w->sb_f = 1;
+  if (!pre && w->ok && n * (long long)(12 + val_bytes) > (48ll << 20)) {
+    // (CTA, super-bucket) runs of >= ~256 elements; <= 4096 buckets each
+    const long long max_sb = std::max(1ll, n / (256ll * kMaxGrid / 2));
+    const long long f = std::min(4096ll, (w->n_cb + max_sb - 1) / max_sb);
+    if (f >= 2) w->sb_f = (int)f;
+  }
+  w->n_sb = (w->n_cb + w->sb_f - 1) / w->sb_f;
+  w->sb_cnt = c.take<unsigned>(std::max(1ll, w->n_sb));
+  w->sb_fill = c.take<unsigned>(w->sb_f > 1 ? w->n_cb : 1);
   w->zero_bytes = c.off;
   w->cb_start = c.take<long long>(w->n_cb + 1);
   w->cb_col = c.take<unsigned>(w->n_cb + 1);
@@ -89,14 +107,15 @@ static size_t carve_persist(Carve& c, PersistWs* w, long long n, long long n_col
   w->col_kept = c.take<unsigned>(std::max(1ll, n_cols));
   w->cta_sums = c.take<long long>(kMaxGrid);
   w->own_info = c.take<long long>(2);
+  w->vals_alt = w->sb_f > 1 ? (void*)c.take<char>(n1 * (long long)val_bytes) : nullptr;
   return c.off;
 }
 
-template <class T, class S1, class S2>
-static int launch_persist(PersistArgs<T, S1, S2>& a, cudaStream_t st) {
+template <class T, class S1, class S2, bool kTwo>
+static int launch_persist_k(PersistArgs<T, S1, S2>& a, cudaStream_t st) {
   static int grid_of[kMaxDevices] = {0};  // per device: the attribute and occupancy are per device
   const size_t smem = sizeof(PersistSmem<T>);
-  auto kern = persist_bucket_kernel<T, S1, S2>;
+  auto kern = persist_bucket_kernel<T, S1, S2, kTwo>;
   int dev = 0;
   AS_CUDA_TRY(cudaGetDevice(&dev));
   AS_REQUIRE(dev >= 0 && dev < kMaxDevices, AS_ERR_CUDA, "device ordinal %d beyond %d", dev, kMaxDevices);
@@ -112,6 +131,15 @@ static int launch_persist(PersistArgs<T, S1, S2>& a, cudaStream_t st) {
   void* args[] = {(void*)&a};
   AS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSegThreads), args, smem, st));
   return AS_OK;
+}
+
+template <class T, class S1, class S2>
+static int launch_persist(PersistArgs<T, S1, S2>& a, cudaStream_t st) {
+  constexpr bool kPre = std::is_same<S1, NoSrc<T>>::value && std::is_same<S2, NoSrc<T>>::value;
+  if constexpr (!kPre) {
+    if (a.sb_f > 1) return launch_persist_k<T, S1, S2, true>(a, st);
+  }
+  return launch_persist_k<T, S1, S2, false>(a, st);
 }
 
 // Launch the persistent kernel on an already carved workspace.  pre_ptr !=
@@ -160,6 +188,11 @@ static int run_persist_ws(PersistWs& w, const S1& s1, const S2& s2, long long n,
   a.cb_col = w.cb_col;
   a.order = pre_ptr ? w.order : nullptr;
   a.tstate = w.tstate;
+  a.sb_f = w.sb_f;
+  a.n_sb = w.n_sb;
+  a.sb_cnt = w.sb_cnt;
+  a.sb_fill = w.sb_fill;
+  a.vals_alt = (T*)w.vals_alt;
   static unsigned long long* dbg_ts = nullptr;
   const bool phase_dbg = getenv("AS_PHASE_TIMES") != nullptr;
   if (phase_dbg) {

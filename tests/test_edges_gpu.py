@@ -179,3 +179,16 @@ def test_spmm_chunk_remainders_empty_rows(K, rng, k):
     got = K.spmm(n_rows, n_cols, csr, torch.as_tensor(np.asfortranarray(X), device=DEV)).cpu().numpy()
     want = oracle.spmm(*a, X, n_rows, n_cols)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("shape", [(200_000, 300_000, 3_000_000), (5_000, 2_000_000, 4_000_000)])
+def test_build_and_transpose_two_level_scatter(K, rng, shape):
+    # element data beyond L2: the two-level (super-bucket) scatter path
+    n_rows, n_cols, n = shape
+    rows, cols = rng.integers(0, n_rows, n), rng.integers(0, n_cols, n)
+    vals = rng.uniform(-1, 1, n)
+    got = _build(K, n_rows, n_cols, rows, cols, vals)
+    want = oracle.canonicalize(n_rows, n_cols, rows, cols, vals)
+    assert_csc_equal(got, want, exact_values=True)
+    t = K.transpose(n_rows, n_cols, *_csc(want))
+    assert_csc_equal(_np(t), oracle.transpose(n_rows, n_cols, *want), exact_values=True)
