@@ -245,6 +245,9 @@ struct NoSrc {
 };
 
 // ------------------------------------------------------------------------
+#ifndef AS_PERSIST_MINB
+#define AS_PERSIST_MINB 2  // CTAs per SM the register allocation is sized for
+#endif
 constexpr int kMaxCoarse = 8192;  // coarse buckets (two u32 arrays in smem)
 constexpr int kMaxW = 1024;       // columns per coarse bucket
 constexpr int kTBins = 1024;      // second-level bins per bucket tile
@@ -783,7 +786,7 @@ __device__ long long process_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1
 }
 
 template <class T, class S1, class S2, bool kTwo = false>
-__global__ void __launch_bounds__(kSegThreads, 3) persist_bucket_kernel(PersistArgs<T, S1, S2> a) {
+__global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_kernel(PersistArgs<T, S1, S2> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PersistSmem<T>& SM = *reinterpret_cast<PersistSmem<T>*>(smem_raw);
   BTileSmem<T>& S = SM.t;

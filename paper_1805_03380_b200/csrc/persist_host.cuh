@@ -41,19 +41,20 @@ struct PersistWs {
 };
 
 // Coarse buckets of ~n_cols / n_cb consecutive output columns (bucket(c) =
-// (c * cb_mul) >> 32).  n_cb: ~0.8 * kCap elements per bucket on average,
-// rounded up to whole waves of the co-resident grid (kNumSMs x 3 CTAs) when
-// above one wave, so the tile phase has no half-empty last wave; at least n_cols / kMaxBucketCols
+// (c * cb_mul) >> 32).  n_cb: ~0.9 * kCap elements per bucket on average,
+// rounded up to whole waves of the co-resident grid (kNumSMs x AS_PERSIST_MINB
+// CTAs) when above one wave, so the tile phase has no half-empty last wave
+// (AS_FILL / AS_WAVES override, for sweeps); at least n_cols / kMaxBucketCols
 // (a bucket's columns index shared arrays), at most kMaxCoarse.  Returns 0
 // when the column count exceeds kMaxCoarse * kMaxBucketCols.
 constexpr long long kMaxBucketCols = kMaxW - 24;
 
 static inline long long choose_ncb(long long n, long long n_cols) {
-  static const double kFill = getenv("AS_FILL") ? atof(getenv("AS_FILL")) : 0.8;
-  const long long wave = (long long)kNumSMs * 3;
+  static const double kFill = getenv("AS_FILL") ? atof(getenv("AS_FILL")) : 0.9;
+  const long long wave = (long long)kNumSMs * AS_PERSIST_MINB;
   long long nb = (long long)((double)n / (kFill * kCap)) + 1;
-  static const bool kWaves = getenv("AS_WAVES") ? atoi(getenv("AS_WAVES")) != 0 : true;
-  if (kWaves && nb > wave) nb = (nb + wave - 1) / wave * wave;  // below one wave: fewer, fuller tiles
+  static const int kWaves = getenv("AS_WAVES") ? atoi(getenv("AS_WAVES")) : 1;
+  if (kWaves == 2 || (kWaves == 1 && nb > wave)) nb = (nb + wave - 1) / wave * wave;
   nb = std::max(nb, (n_cols + kMaxBucketCols - 1) / kMaxBucketCols);
   nb = std::min(nb, std::max(1ll, n_cols));
   nb = std::min(nb, (long long)kMaxCoarse);

@@ -12,7 +12,10 @@
 
 namespace as {
 
-constexpr int kSegThreads = 256;            // threads of a tile CTA
+#ifndef AS_SEG_THREADS
+#define AS_SEG_THREADS 512
+#endif
+constexpr int kSegThreads = AS_SEG_THREADS;  // threads of a tile CTA
 constexpr int kCap = 2048;                  // elements of a shared-memory tile
 constexpr int kItems = kCap / kSegThreads;  // 8 positions per thread
 constexpr int kWarpSortMax = 512;           // bins up to this sort in one warp
