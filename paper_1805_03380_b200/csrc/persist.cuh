@@ -44,6 +44,21 @@ namespace as {
     if ((a).phase_ts && blockIdx.x == 0 && threadIdx.x == 0) (a).phase_ts[gen] = global_ns();   \
   } while (0)
 
+// Tile-step timers (diagnostic build only, -DAS_TILE_TIMES): thread 0 of
+// block 0 accumulates clock64 cycles per step of the tile loop in g_tt.
+#ifdef AS_TILE_TIMES
+__device__ unsigned long long g_tt[33];
+AS_DEVICE_INLINE void tt_mark(int i) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long n = clock64();
+    if (i >= 0) g_tt[i] += n - g_tt[32];
+    g_tt[32] = n;
+  }
+}
+#else
+AS_DEVICE_INLINE void tt_mark(int) {}
+#endif
+
 // ------------------------------------------------------------------------
 // element sources: visit(p, P, report, f) calls f(col, row, idx, i) for every
 // valid element of chunk p of P (the same partition every time it is called)
@@ -286,7 +301,7 @@ struct PersistArgs {
   // taken in `order` (largest size class first)
   unsigned* cb_col;              // [n_cb + 1]
   unsigned* order;               // [n_cb] (pre_ptr mode only)
-  unsigned long long* tstate;    // [n_cb] zeroed: chained-scan states of the buckets' kept counts
+  unsigned long long* tstate;    // zeroed: [n_cb] bucket kept counts, then [n_cb / 32 + 1] group words
   // two-level scatter (large inputs): super-buckets of sb_f consecutive buckets
   int sb_f;                      // buckets per super-bucket (<= 1: single level)
   long long n_sb;
@@ -457,6 +472,7 @@ __device__ long long bucket_chunk_reduce(BTileSmem<T>& S, long long b, int cm, l
     if (lane == 0 && base + warp * 32 < cm) S.hbits[(base >> 5) + warp] = hb;
   }
   __syncthreads();
+  tt_mark(8);
   const int pb = tid * kItems, pe = min(pb + kItems, cm);
   int cnt = 0;
   for (int p = pb; p < pe; p++) {
@@ -500,6 +516,7 @@ __device__ long long bucket_chunk_reduce(BTileSmem<T>& S, long long b, int cm, l
   }
   if (tid == 0) S.v.excl[cm] = (unsigned short)total;
   __syncthreads();
+  tt_mark(9);
   return total;
 }
 
@@ -539,6 +556,7 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int Wt, int row_bits) {
     }
   }
   __syncthreads();
+  tt_mark(2);
   const unsigned long long cmin = S.cmin, cmax = S.cmax;
   int sh = 0;
   while (sh < row_bits && (cmax >> sh) - (cmin >> sh) + 1 > (unsigned long long)kTBins) sh++;
@@ -552,6 +570,7 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int Wt, int row_bits) {
   __syncthreads();
   for (int p = tid; p < m; p += nthr) atomicAdd(&S.v.bk.cursor[bin_of(p)], 1u);
   __syncthreads();
+  tt_mark(3);
   {
     constexpr int kPer = kTBins / kSegThreads;
     const int b0 = tid * kPer;
@@ -575,6 +594,7 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int Wt, int row_bits) {
     if (tid == 0) S.v.bk.bstart[nbins] = (unsigned short)m;
   }
   __syncthreads();
+  tt_mark(4);
   for (int p = tid; p < m; p += nthr) {
     const int b = bin_of(p);
     const unsigned slot = atomicAdd(&S.v.bk.cursor[b], 1u);
@@ -591,6 +611,7 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int Wt, int row_bits) {
     S.cstart[l] = S.v.bk.bstart[bl < 0 ? 0 : (bl > nbins ? nbins : bl)];
   }
   __syncthreads();
+  tt_mark(5);
   for (int b = tid; b < nbins; b += nthr) {
     const int L = S.v.bk.bstart[b + 1] - S.v.bk.bstart[b];
     if (L > kRankMax && L <= kWarpSortMax) S.med[atomicAdd(&S.n_med, 1)] = (short)b;
@@ -609,6 +630,7 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int Wt, int row_bits) {
     }
   }
   __syncthreads();
+  tt_mark(6);
   const int n_med = S.n_med, n_big = S.n_big;
   for (int q = warp; q < n_med; q += nwarps) {
     const int b = S.med[q];
@@ -632,6 +654,7 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int Wt, int row_bits) {
     __syncthreads();
   }
   __syncthreads();
+  tt_mark(7);
 }
 
 // A bucket larger than the tile: split it in global memory into bins of
@@ -783,6 +806,49 @@ __device__ long long process_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1
   for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = S.ckept[l];
   __syncthreads();
   return run_base;
+}
+
+// Executed by one full warp of the tile: the exclusive prefix of bucket t's
+// kept count over buckets [0, t).  Each bucket publishes its count to st[t]
+// and adds it to its group word grp[t / 32] (publishers << 56 | sum); the
+// prefix is the completed words of the preceding groups plus the in-group
+// predecessors -- two parallel polls.  (A chained look-back walked back up to
+// n_cb / 32 serial rounds: the tiles of a wave reach this point together, so
+// few inclusive prefixes were ever published in time.)  Tickets are handed
+// out in bucket order by co-resident CTAs, so every predecessor is running.
+__device__ __forceinline__ unsigned long long group_lookback_warp(unsigned long long* st, unsigned long long* grp,
+                                                                  long long t, unsigned long long kept) {
+  const int lane = threadIdx.x & 31;
+  constexpr unsigned long long kOne = 1ull << 56, kSum = kOne - 1;
+  if (lane == 0) {
+    atomicExch(&st[t], (kept << 1) | 1ull);
+    atomicAdd(&grp[t >> 5], kOne | kept);
+  }
+  unsigned long long pre = 0;
+  const long long q = (t & ~31ll) + lane;  // in-group predecessor of this lane
+  if (q < t) {
+    unsigned long long s;
+    do {
+      s = tile_peek(&st[q]);
+    } while (!(s & 1ull));
+    pre = s >> 1;
+  }
+  const long long ng = t >> 5;  // complete groups before t's
+  for (long long i0 = 0; i0 < ng; i0 += 32 * 4) {
+    unsigned long long v[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const long long i = i0 + lane + 32 * u;
+      v[u] = i < ng ? tile_peek(&grp[i]) : 32 * kOne;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const long long i = i0 + lane + 32 * u;
+      while ((v[u] >> 56) < 32) v[u] = tile_peek(&grp[i]);
+      pre += v[u] & kSum;
+    }
+  }
+  return warp_reduce_sum(pre);
 }
 
 template <class T, class S1, class S2, bool kTwo = false>
@@ -1017,6 +1083,7 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
   }
 
   // ---------------- phase 4: bucket tiles ----------------
+  tt_mark(-1);
   while (true) {
     if (tid == 0) {
       long long t = (long long)atomicAdd(a.ticket, 1u);
@@ -1030,6 +1097,7 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
       }
     }
     __syncthreads();
+    tt_mark(0);
     const long long t = S.tile;
     if (t >= ncb) break;
     const long long s = S.s, m = S.m;
@@ -1042,7 +1110,7 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
     // them: its largest-first tile order would break the look-back chain)
     auto lookback = [&](long long kept) -> long long {
       if (tid < 32) {
-        const unsigned long long pre = tile_lookback_warp(a.tstate, t, (unsigned long long)kept);
+        const unsigned long long pre = group_lookback_warp(a.tstate, a.tstate + ncb, t, (unsigned long long)kept);
         if (tid == 0) S.prefix = (long long)pre;
       }
       __syncthreads();
@@ -1083,6 +1151,7 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
         }
       }
       __syncthreads();
+      tt_mark(1);
       sort_bucket_smem(S, (int)m, Wt, a.row_bits);
       bucket_chunk_reduce<T>(S, 0, (int)m, m, nullptr, nullptr, col_base, a.vs, a.mode, a.prune, a.vals_b + s);
       if constexpr (kPre) {
@@ -1097,6 +1166,7 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
           a.col_kept[col_base + l] = S.v.excl[S.cstart[l + 1]] - S.v.excl[S.cstart[l]];
       } else {
         const long long base = lookback((long long)S.v.excl[m]);
+        tt_mark(10);
         for (int p = tid; p < m; p += nthr) {
           const unsigned e0 = S.v.excl[p], e1 = S.v.excl[p + 1];
           if (e1 != e0) {
@@ -1125,6 +1195,7 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
       }
     }
     __syncthreads();
+    tt_mark(11);
   }
   if constexpr (!kPre) {
     AS_PHASE_MARK(a, gen + 1);

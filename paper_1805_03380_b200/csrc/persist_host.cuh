@@ -79,7 +79,8 @@ static size_t carve_persist(Carve& c, PersistWs* w, long long n, long long n_col
   }
   w->zero = c.take<unsigned>(64);
   w->cb_cnt = c.take<unsigned>(std::max(1ll, w->n_cb));  // pre: size class and slot of each bucket
-  w->tstate = c.take<unsigned long long>(std::max(1ll, w->n_cb));
+  // bucket states, then one word per group of 32 buckets (group_lookback_warp)
+  w->tstate = c.take<unsigned long long>(std::max(1ll, w->n_cb) + (w->n_cb + 31) / 32 + 1);
   // two-level scatter when the scattered element data outgrows L2 and a
   // (CTA, bucket) run would be short: super-buckets of sb_f buckets so a
   // (CTA, super-bucket) run averages >= 32 elements
@@ -200,6 +201,10 @@ static int run_persist_ws(PersistWs& w, const S1& s1, const S2& s2, long long n,
     if (!dbg_ts) AS_CUDA_TRY(cudaMalloc(&dbg_ts, 16 * sizeof(unsigned long long)));
     AS_CUDA_TRY(cudaMemsetAsync(dbg_ts, 0, 16 * sizeof(unsigned long long), st));
     a.phase_ts = dbg_ts;
+#ifdef AS_TILE_TIMES
+    unsigned long long z[33] = {0};
+    AS_CUDA_TRY(cudaMemcpyToSymbolAsync(g_tt, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
+#endif
   }
   const int rc = launch_persist<T, S1, S2>(a, st);
   if (phase_dbg && rc == AS_OK) {
@@ -213,6 +218,14 @@ static int run_persist_ws(PersistWs& w, const S1& s1, const S2& s2, long long n,
         last = i;
       }
     fprintf(stderr, " us\n");
+#ifdef AS_TILE_TIMES
+    unsigned long long tt[33];
+    AS_CUDA_TRY(cudaMemcpyFromSymbolAsync(tt, g_tt, sizeof(tt), 0, cudaMemcpyDeviceToHost, st));
+    AS_CUDA_TRY(cudaStreamSynchronize(st));
+    fprintf(stderr, "[tile steps, block 0, kcycles]");
+    for (int i = 0; i < 12; i++) fprintf(stderr, " %d:%.1f", i, tt[i] * 1e-3);
+    fprintf(stderr, "\n");
+#endif
   }
   return rc;
 }
