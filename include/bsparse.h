@@ -60,6 +60,21 @@ int as_coo_to_csc_f32(int64_t n_rows, int64_t n_cols, int64_t n, const void *row
                       float *out_vals, int64_t *info, void *ws, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * Host side of the end-to-end construction (csrc/upload.cu, host code).
+ * Moves int64 host triplets (csc.py:63-67 index type) to the device as
+ * int32 indices: the values' copy is enqueued first, host threads narrow
+ * rows / cols into pinned staging (n_chunks pieces, each copied as soon as it
+ * is narrowed) -- 16 instead of 24 bytes per triplet over PCIe.  An index
+ * outside [0, 2^31) becomes -1, which as_coo_to_csc_* then reports as the
+ * first out-of-range triplet.  Synchronous on the host for the narrowing,
+ * asynchronous on `stream` for the copies; the staging must not be reused
+ * before they complete.  vals == NULL: only the indices are moved.
+ */
+int as_upload_coo_i64(const int64_t *rows, const int64_t *cols, const void *vals, int64_t n, int64_t val_bytes,
+                      int32_t *stage_rows, int32_t *stage_cols, int32_t *d_rows, int32_t *d_cols, void *d_vals,
+                      int n_threads, int n_chunks, void *stream);
+
+/* ---------------------------------------------------------------------------
  * Insertion-cache flush: base CSC + element-write log -> canonical CSC.
  * Replaces rbt.to_csc (rbt.py:444-458) of the tree that RbtStore.insert
  * (rbt.py:371-387: overwrite; 0.0 erases, :374-376) built on top of

@@ -11,6 +11,9 @@ device->host copy (the only synchronisation).  There is no CPU path.
 
 from __future__ import annotations
 
+import os
+import threading
+
 import torch
 
 from . import _lib
@@ -30,6 +33,57 @@ def _dev(device=None):
 def _read_info(info):
     nnz, bad = (int(x) for x in info.cpu().tolist())
     return nnz, bad
+
+
+_upload_lock = threading.Lock()
+_upload_stage = {"buf": None, "event": None}
+
+
+def _upload_threads():
+    env = os.environ.get("AS_UPLOAD_THREADS")
+    if env:
+        return max(1, int(env))
+    try:
+        return max(1, min(16, len(os.sched_getaffinity(0))))
+    except AttributeError:
+        return max(1, min(16, os.cpu_count() or 1))
+
+
+def upload_coo(rows, cols, vals, device=None):
+    """int64 host triplets -> device (int32 rows, int32 cols, vals) through
+    as_upload_coo_i64: host threads narrow the indices into pinned staging
+    while the values are copied, so 16 bytes per triplet cross PCIe instead
+    of 24.  rows / cols: contiguous CPU int64 tensors (pinned or not); vals:
+    CPU float tensor (pinned: copied by the same call).  An index outside
+    [0, 2^31) arrives as -1 (coo_to_csc reports it as out of range)."""
+    L = _lib.lib()
+    dev = _dev(device)
+    n = int(rows.shape[0])
+    assert rows.dtype == torch.int64 and cols.dtype == torch.int64 and not rows.is_cuda and not cols.is_cuda
+    assert int(cols.shape[0]) == n and int(vals.shape[0]) == n
+    rows, cols, vals = rows.contiguous(), cols.contiguous(), vals.contiguous()
+    d_rows = torch.empty(n, dtype=torch.int32, device=dev)
+    d_cols = torch.empty(n, dtype=torch.int32, device=dev)
+    pinned_vals = vals.is_pinned()
+    d_vals = torch.empty(n, dtype=vals.dtype, device=dev) if pinned_vals else vals.to(dev)
+    if n == 0:
+        return d_rows, d_cols, d_vals
+    with _upload_lock:
+        st = _upload_stage
+        if st["event"] is not None:
+            st["event"].synchronize()  # the previous call's copies have left the staging
+        if st["buf"] is None or st["buf"].numel() < 2 * n:
+            st["buf"] = torch.empty(2 * n, dtype=torch.int32).pin_memory()
+        buf = st["buf"]
+        chunks = int(os.environ.get("AS_UPLOAD_CHUNKS", "4"))
+        with torch.cuda.device(dev):
+            check(L.as_upload_coo_i64(ptr(rows), ptr(cols), ptr(vals) if pinned_vals else None, n,
+                                      vals.element_size(), ptr(buf), buf.data_ptr() + 4 * n, ptr(d_rows),
+                                      ptr(d_cols), ptr(d_vals), _upload_threads(), chunks, stream()))
+            ev = torch.cuda.Event()
+            ev.record()
+        st["event"] = ev
+    return d_rows, d_cols, d_vals
 
 
 def coo_to_csc(n_rows, n_cols, rows, cols, vals, dup=DUP_SUM, out=None):

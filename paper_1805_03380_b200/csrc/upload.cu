@@ -1,0 +1,145 @@
+// upload.cu -- host side of the end-to-end construction path
+// (SpMat.from_triplets / csc.canonicalize on host arrays, csc.py:148-222).
+//
+// The reference takes int64 row / column arrays (csc.py:63-67); the device
+// path indexes in int32.  Instead of moving 24 bytes per triplet over PCIe
+// and narrowing on the device, a pool of host threads narrows the indices
+// into pinned int32 staging while the copy engine moves the values, then the
+// narrowed chunks follow: 16 bytes per triplet on the wire, the narrowing
+// hidden behind the value transfer.  An index outside [0, 2^31) becomes -1,
+// so the build kernel still reports the first out-of-range triplet by its
+// input position (csc.py:215-221 CoordinateError semantics).
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "capi_util.cuh"
+
+namespace as {
+namespace {
+
+// Persistent workers: a job is published by bumping `gen_`; workers spin for
+// a while (back-to-back calls find them awake) and then block on a condition
+// variable.  The caller runs share 0 itself.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool p;
+    return p;
+  }
+
+  void run(int shares, const std::function<void(int)>& fn) {
+    std::lock_guard<std::mutex> call_lock(call_mu_);  // one job at a time
+    ensure(shares - 1);
+    const int helpers = shares - 1;
+    if (helpers > 0) {
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        job_ = &fn;
+        helpers_ = helpers;
+        done_.store(0, std::memory_order_relaxed);
+        gen_.fetch_add(1, std::memory_order_release);
+      }
+      cv_.notify_all();
+    }
+    fn(0);
+    while (done_.load(std::memory_order_acquire) < helpers) {
+    }
+  }
+
+ private:
+  HostPool() = default;
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      gen_.fetch_add(1, std::memory_order_release);
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+
+  void ensure(int n) {
+    while ((int)workers_.size() < n) {
+      const int id = (int)workers_.size() + 1;
+      workers_.emplace_back([this, id] { loop(id); });
+    }
+  }
+
+  void loop(int id) {
+    unsigned long long seen = 0;
+    while (true) {
+      unsigned long long g = gen_.load(std::memory_order_acquire);
+      for (long spin = 0; g == seen && spin < (1l << 21); spin++) g = gen_.load(std::memory_order_acquire);
+      if (g == seen) {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+        g = gen_.load(std::memory_order_acquire);
+      }
+      const std::function<void(int)>* job;
+      int helpers;
+      {  // the job and its generation together: a lagging worker runs the
+         // current job once and never re-runs it
+        std::lock_guard<std::mutex> lk(mu_);
+        if (stop_) return;
+        job = job_;
+        helpers = helpers_;
+        seen = gen_.load(std::memory_order_acquire);
+      }
+      if (id <= helpers) {
+        (*job)(id);
+        done_.fetch_add(1, std::memory_order_acq_rel);
+      }
+    }
+  }
+
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_;
+  std::vector<std::thread> workers_;
+  const std::function<void(int)>* job_ = nullptr;
+  int helpers_ = 0;
+  bool stop_ = false;
+  std::atomic<unsigned long long> gen_{0};
+  std::atomic<int> done_{0};
+};
+
+inline int32_t narrow_index(int64_t v) { return (v >= 0 && v <= 0x7fffffffll) ? (int32_t)v : -1; }
+
+}  // namespace
+}  // namespace as
+
+using namespace as;
+
+extern "C" {
+
+int as_upload_coo_i64(const int64_t* rows, const int64_t* cols, const void* vals, int64_t n, int64_t val_bytes,
+                      int32_t* stage_rows, int32_t* stage_cols, int32_t* d_rows, int32_t* d_cols, void* d_vals,
+                      int n_threads, int n_chunks, void* stream) {
+  cudaStream_t st = S(stream);
+  AS_REQUIRE(n >= 0 && (val_bytes == 4 || val_bytes == 8), AS_ERR_ARG, "bad upload arguments");
+  if (n == 0) return AS_OK;
+  const int T = std::max(1, std::min(n_threads, 256));
+  const int K = (int)std::max<int64_t>(1, std::min<int64_t>(n_chunks, (n + 65535) / 65536));
+  // the values first: the copy engine moves them while the indices are
+  // narrowed (vals == nullptr: the caller moves them)
+  if (vals) AS_CUDA_TRY(cudaMemcpyAsync(d_vals, vals, (size_t)(n * val_bytes), cudaMemcpyHostToDevice, st));
+  const int64_t per = (n + K - 1) / K;
+  for (int k = 0; k < K; k++) {
+    const int64_t lo = (int64_t)k * per, hi = std::min(n, lo + per);
+    if (lo >= hi) break;
+    const int64_t span = hi - lo;
+    HostPool::get().run(T, [&](int w) {
+      const int64_t a = lo + span * w / T, b = lo + span * (w + 1) / T;
+      for (int64_t i = a; i < b; i++) stage_rows[i] = narrow_index(rows[i]);
+      for (int64_t i = a; i < b; i++) stage_cols[i] = narrow_index(cols[i]);
+    });
+    AS_CUDA_TRY(cudaMemcpyAsync(d_rows + lo, stage_rows + lo, (size_t)span * 4, cudaMemcpyHostToDevice, st));
+    AS_CUDA_TRY(cudaMemcpyAsync(d_cols + lo, stage_cols + lo, (size_t)span * 4, cudaMemcpyHostToDevice, st));
+  }
+  return AS_OK;
+}
+
+}  // extern "C"

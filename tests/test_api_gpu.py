@@ -329,3 +329,34 @@ def test_canonicalize_host_zero_copy():
     m = C.canonicalize_host(Dims(2, 3), np.array([1, 1, 0, 1]), np.array([0, 0, 2, 0]),
                             np.array([2.0, 3.0, 9.0, 4.0]), C.DUP_LAST, out=out)
     assert m.get(1, 0) == 4.0 and m.get(0, 2) == 9.0 and m.nnz == 2
+
+
+def test_int64_host_upload_narrowing():
+    """Host int64 triplets take the narrowing upload (as_upload_coo_i64):
+    pinned and pageable inputs, chunk edges, and indices that do not fit
+    int32 (2^32 + r, negatives) reported as the first bad triplet -- the
+    same CoordinateError index as the device path."""
+    from paper_1805_03380_b200 import _kernels
+
+    rng = np.random.default_rng(77)
+    for (r, c, n) in [(300, 200, 5000), (7, 5, 1), (10000, 10000, 300001), (50, 40, 0)]:
+        rows, cols, vals = rng.integers(0, r, n), rng.integers(0, c, n), rng.uniform(-1, 1, n)
+        want = oracle.canonicalize(r, c, rows, cols, vals)
+        for pinned in (False, True):
+            args = (rows, cols, vals)
+            if pinned:
+                args = tuple(torch.from_numpy(a).pin_memory() for a in args)
+            m = SpMat.from_triplets(r, c, args).csc()
+            assert np.array_equal(m.col_offsets, want[2]) and np.array_equal(m.row_indices, want[1])
+            assert np.array_equal(m.values.view(np.int64), want[0].view(np.int64))
+    # direct: narrowed indices, -1 for anything outside [0, 2^31)
+    rows = np.array([3, (1 << 32) + 3, -5, (1 << 31) - 1, 1 << 31], dtype=np.int64)
+    d_r, d_c, d_v = _kernels.upload_coo(torch.from_numpy(rows), torch.from_numpy(rows.copy()),
+                                        torch.arange(5, dtype=torch.float64))
+    assert d_r.cpu().tolist() == [3, -1, -1, (1 << 31) - 1, -1] and d_c.cpu().tolist() == d_r.cpu().tolist()
+    assert d_v.cpu().tolist() == [0.0, 1.0, 2.0, 3.0, 4.0]
+    for bad_pos, bad_val in [(2, (1 << 32) + 1), (4, -1), (0, 1 << 40)]:
+        rows = np.zeros(6, dtype=np.int64)
+        rows[bad_pos] = bad_val
+        with pytest.raises(CoordinateError, match="triplet %d " % bad_pos):
+            SpMat.from_triplets(4, 4, (rows, np.zeros(6, dtype=np.int64), np.ones(6)))
