@@ -44,9 +44,11 @@ def _upload_threads():
     if env:
         return max(1, int(env))
     try:
-        return max(1, min(16, len(os.sched_getaffinity(0))))
+        cores = len(os.sched_getaffinity(0))
     except AttributeError:
-        return max(1, min(16, os.cpu_count() or 1))
+        cores = os.cpu_count() or 1
+    # half the cores, at most 8: a descheduled helper stalls the whole call
+    return max(1, min(8, cores // 2))
 
 
 def upload_coo(rows, cols, vals, device=None):

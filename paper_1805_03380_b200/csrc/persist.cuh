@@ -296,6 +296,7 @@ struct PersistArgs {
   unsigned* ticket;
   GridBar gb;
   unsigned long long* phase_ts;  // optional: globaltimer after each phase (debug)
+  int stage;                     // 1: phase 3 stages each CTA's chunk in shared memory (stage_layout)
   const long long* pre_ptr;      // non-null: input already bucketed by column (SpGEMM products)
   // bucket t spans columns [cb_col[t], cb_col[t+1]); pre_ptr mode: tiles are
   // taken in `order` (largest size class first)
@@ -352,15 +353,31 @@ struct BTileSmem {
   int wt;
 };
 
+// Dynamic shared memory of the persistent kernel: two CTAs per SM (the
+// register file is the binding limit), so ~110 KB each is free to use.
+constexpr int kPersistSmemBytes = 110 * 1024;
+
+// Phases 1-3: colc, then three runtime-sized [n_cb] arrays (histogram /
+// cursor, the CTA's range inside each bucket, the CTA-local bucket offsets),
+// then the scatter staging (stage_layout).  Phase 4: the tile.
 template <class T>
 union PersistSmem {
   struct {
-    unsigned a[kMaxCoarse];  // histogram, then shared cursor
-    unsigned b[kMaxCoarse];  // CTA range inside each bucket, then slot base
     int colc[kColCache + 1];
+    unsigned ab[3 * kMaxCoarse];
   } h;
   BTileSmem<T> t;
+  unsigned char raw[kPersistSmemBytes];
 };
+
+// Scatter staging behind the [3 * n_cb] arrays: keys, values, columns of the
+// CTA's chunk in local bucket order.  Returns the capacity in elements.
+template <class T>
+__host__ __device__ inline long long stage_layout(long long ncb, long long* off) {
+  const long long o = ((long long)sizeof(int) * (kColCache + 1) + 12ll * ncb + 15) & ~15ll;
+  *off = o;
+  return o >= kPersistSmemBytes ? 0 : (kPersistSmemBytes - o) / (long long)(12 + sizeof(T));
+}
 
 AS_DEVICE_INLINE void cta_range(long long n, long long g, long long G, long long* lo, long long* hi) {
   const long long per = (n + G - 1) / G;
@@ -867,6 +884,9 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
   // transpose: separate instantiations, each without the other's code
   constexpr bool kPre = std::is_same<S1, NoSrc<T>>::value && std::is_same<S2, NoSrc<T>>::value;
   AS_PHASE_MARK(a, 0);
+  unsigned* const ha = SM.h.ab;            // histogram, then cursor
+  unsigned* const hb = SM.h.ab + ncb;      // CTA range inside each bucket, then slot base
+  unsigned* const hl = SM.h.ab + 2 * ncb;  // CTA-local bucket offsets (staged scatter)
   a.s1.set_cache(SM.h.colc);
   a.s2.set_cache(SM.h.colc);
 
@@ -925,10 +945,10 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
     const unsigned long long c0 = cb_mul ? (((unsigned long long)t << 32) + cb_mul - 1) / cb_mul : 0ull;
     a.cb_col[t] = (unsigned)(t == ncb ? a.n_cols : min((long long)c0, a.n_cols));
   }
-  for (long long b = tid; b < ncb; b += nthr) SM.h.a[b] = 0u;
+  for (long long b = tid; b < ncb; b += nthr) ha[b] = 0u;
   __syncthreads();
   {
-    auto inc = [&](unsigned c, unsigned, unsigned long long, long long, T) { atomicAdd(&SM.h.a[bucket_of(c)], 1u); };
+    auto inc = [&](unsigned c, unsigned, unsigned long long, long long, T) { atomicAdd(&ha[bucket_of(c)], 1u); };
     a.s1.visit(g, G, true, inc);
     a.s2.visit(g, G, true, inc);
   }
@@ -941,21 +961,33 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
     // adds its per-bucket counts to the global bucket totals
     for (long long sb = tid; sb < nsb; sb += nthr) {
       unsigned sum = 0;
-      for (long long b = sb * F; b < min(ncb, sb * F + F); b++) sum += SM.h.a[b];
-      SM.h.b[sb] = sum ? atomicAdd(&a.sb_cnt[sb], sum) : 0u;
+      for (long long b = sb * F; b < min(ncb, sb * F + F); b++) sum += ha[b];
+      hb[sb] = sum ? atomicAdd(&a.sb_cnt[sb], sum) : 0u;
     }
     for (long long b = tid; b < ncb; b += nthr) {
-      const unsigned h = SM.h.a[b];
+      const unsigned h = ha[b];
       if (h) atomicAdd(&a.cb_cnt[b], h);
     }
     __syncthreads();
-    for (long long b = tid; b < ncb; b += nthr) SM.h.a[b] = 0u;  // super-bucket cursors
+    for (long long b = tid; b < ncb; b += nthr) ha[b] = 0u;  // super-bucket cursors
   } else {
     for (long long b = tid; b < ncb; b += nthr) {
-      const unsigned h = SM.h.a[b];
-      SM.h.b[b] = h ? atomicAdd(&a.cb_cnt[b], h) : 0u;
-      SM.h.a[b] = 0u;
+      const unsigned h = ha[b];
+      hb[b] = h ? atomicAdd(&a.cb_cnt[b], h) : 0u;
     }
+    if (a.stage) {  // local offsets of the staged scatter: scan of this CTA's counts
+      __syncthreads();
+      long long running = 0;
+      for (long long cb = 0; cb < ncb; cb += nthr) {
+        const long long b = cb + tid;
+        long long ctot;
+        const long long ex = block_exclusive_scan<long long>(b < ncb ? (long long)ha[b] : 0ll, xscan, &ctot);
+        if (b < ncb) hl[b] = (unsigned)(running + ex);
+        running += ctot;
+      }
+    }
+    __syncthreads();
+    for (long long b = tid; b < ncb; b += nthr) ha[b] = 0u;
   }
   grid_sync(a.gb, gen);
   AS_PHASE_MARK(a, gen);
@@ -970,9 +1002,9 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
       const long long ex = block_exclusive_scan<long long>(cnt, xscan, &ctot);
       if (b < ncb) {
         if constexpr (kTwo) {
-          if (b % F == 0) SM.h.b[b / F] += (unsigned)(running + ex);  // super-bucket start
+          if (b % F == 0) hb[b / F] += (unsigned)(running + ex);  // super-bucket start
         } else {
-          SM.h.b[b] += (unsigned)(running + ex);  // slot base of this CTA's range
+          hb[b] += (unsigned)(running + ex);  // slot base of this CTA's range
         }
         if (g == 0) a.cb_start[b] = running + ex;
       }
@@ -987,7 +1019,7 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
     // 3a: into super-bucket order (alt arrays)
     auto put = [&](unsigned c, unsigned minor, unsigned long long idx, long long, T v) {
       const unsigned sb = bucket_of(c) / (unsigned)F;
-      const unsigned slot = SM.h.b[sb] + atomicAdd(&SM.h.a[sb], 1u);
+      const unsigned slot = hb[sb] + atomicAdd(&ha[sb], 1u);
       a.keys_alt[slot] = ((unsigned long long)minor << 32) | idx;
       a.colb_alt[slot] = c;
       a.vals_alt[slot] = v;
@@ -1017,7 +1049,7 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
       __syncthreads();
       const long long bb = S.tile;
       const long long nbk = min(ncb - bb, 2ll * F);
-      for (long long f = tid; f < nbk; f += nthr) SM.h.a[f] = 0u;
+      for (long long f = tid; f < nbk; f += nthr) ha[f] = 0u;
       __syncthreads();
       constexpr int kU = 8;  // loads of kU elements in flight per thread
       for (long long i0 = lo + tid; i0 < hi; i0 += (long long)kU * nthr) {
@@ -1029,13 +1061,13 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
         }
 #pragma unroll
         for (int u = 0; u < kU; u++)
-          if (i0 + (long long)u * nthr < hi) atomicAdd(&SM.h.a[bucket_of(cc[u]) - bb], 1u);
+          if (i0 + (long long)u * nthr < hi) atomicAdd(&ha[bucket_of(cc[u]) - bb], 1u);
       }
       __syncthreads();
       for (long long f = tid; f < nbk; f += nthr) {
-        const unsigned h = SM.h.a[f];
-        SM.h.b[f] = h ? (unsigned)__ldcg(&a.cb_start[bb + f]) + atomicAdd(&a.sb_fill[bb + f], h) : 0u;
-        SM.h.a[f] = 0u;
+        const unsigned h = ha[f];
+        hb[f] = h ? (unsigned)__ldcg(&a.cb_start[bb + f]) + atomicAdd(&a.sb_fill[bb + f], h) : 0u;
+        ha[f] = 0u;
       }
       __syncthreads();
       for (long long i0 = lo + tid; i0 < hi; i0 += (long long)kU * nthr) {
@@ -1055,24 +1087,53 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
         for (int u = 0; u < kU; u++) {
           if (i0 + (long long)u * nthr >= hi) continue;
           const unsigned f = bucket_of(cc[u]) - (unsigned)bb;
-          const unsigned slot = SM.h.b[f] + atomicAdd(&SM.h.a[f], 1u);
+          const unsigned slot = hb[f] + atomicAdd(&ha[f], 1u);
           a.keys[slot] = kk[u];
           a.colb[slot] = cc[u];
           a.vals_b[slot] = vv[u];
         }
       }
     }
+  } else if (a.stage) {
+    // staged: the chunk is counting-sorted by bucket in shared memory, then
+    // written run by run -- consecutive threads store consecutive slots of a
+    // bucket (the scatter is bound by L2 store transactions, one per
+    // scattered element and array without this)
+    long long off;
+    const long long cap = stage_layout<T>(ncb, &off);
+    unsigned long long* st_k = reinterpret_cast<unsigned long long*>(SM.raw + off);
+    T* st_v = reinterpret_cast<T*>(SM.raw + off + 8 * cap);
+    unsigned* st_c = reinterpret_cast<unsigned*>(SM.raw + off + (8 + sizeof(T)) * cap);
+    auto put = [&](unsigned c, unsigned minor, unsigned long long idx, long long, T v) {
+      const unsigned cb = bucket_of(c);
+      const unsigned q = hl[cb] + atomicAdd(&ha[cb], 1u);
+      st_k[q] = ((unsigned long long)minor << 32) | idx;
+      st_c[q] = c;
+      st_v[q] = v;
+    };
+    a.s1.template visit<true>(g, G, false, put);
+    a.s2.template visit<true>(g, G, false, put);
+    __syncthreads();
+    const unsigned total = ncb > 0 ? hl[ncb - 1] + ha[ncb - 1] : 0u;
+    for (unsigned q = tid; q < total; q += nthr) {
+      const unsigned c = st_c[q];
+      const unsigned cb = bucket_of(c);
+      const unsigned slot = hb[cb] + (q - hl[cb]);
+      a.keys[slot] = st_k[q];
+      a.colb[slot] = c;
+      a.vals_b[slot] = st_v[q];
+    }
   } else {
     a.s1.template visit<true>(g, G, false, [&](unsigned c, unsigned minor, unsigned long long idx, long long, T v) {
       const unsigned cb = bucket_of(c);
-      const unsigned slot = SM.h.b[cb] + atomicAdd(&SM.h.a[cb], 1u);
+      const unsigned slot = hb[cb] + atomicAdd(&ha[cb], 1u);
       a.keys[slot] = ((unsigned long long)minor << 32) | idx;
       a.colb[slot] = c;
       a.vals_b[slot] = v;
     });
     a.s2.template visit<true>(g, G, false, [&](unsigned c, unsigned minor, unsigned long long idx, long long, T v) {
       const unsigned cb = bucket_of(c);
-      const unsigned slot = SM.h.b[cb] + atomicAdd(&SM.h.a[cb], 1u);
+      const unsigned slot = hb[cb] + atomicAdd(&ha[cb], 1u);
       a.keys[slot] = ((unsigned long long)minor << 32) | idx;
       a.colb[slot] = c;
       a.vals_b[slot] = v;

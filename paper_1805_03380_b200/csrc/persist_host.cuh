@@ -130,8 +130,26 @@ static int launch_persist_k(PersistArgs<T, S1, S2>& a, cudaStream_t st) {
     grid_of[dev] = (int)std::min<long long>((long long)per_sm * sms, kMaxGrid);
   }
   const int grid = grid_of[dev];
+  // staged scatter when the largest CTA chunk of the two sources fits
+  auto chunk = [&](long long n) -> long long { return (((n + grid - 1) / grid) + 3) & ~3ll; };
+  long long st_off;
+  a.stage = (!kTwo && a.n_cb <= kMaxCoarse && a.s1.size() + a.s2.size() > 0 &&
+             chunk(a.s1.size()) + chunk(a.s2.size()) <= stage_layout<T>(a.n_cb, &st_off))
+                ? 1
+                : 0;
+  static const bool kNoStage = getenv("AS_NO_STAGE") != nullptr;
+  if (kNoStage) a.stage = 0;
+  // without the staging only the tile / the [3 * n_cb] arrays are needed: the
+  // rest of the 256 KB goes back to L1 (the pre-bucketed SpGEMM tiles gather
+  // through it)
+  constexpr bool kPre = std::is_same<S1, NoSrc<T>>::value && std::is_same<S2, NoSrc<T>>::value;
+  const size_t need = kPre ? sizeof(BTileSmem<T>)
+                      : a.stage ? smem
+                                : std::max(sizeof(BTileSmem<T>),
+                                           (size_t)(((long long)sizeof(int) * (kColCache + 1) + 12ll * a.n_cb + 15) & ~15ll));
   void* args[] = {(void*)&a};
-  AS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSegThreads), args, smem, st));
+  AS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSegThreads), args, std::min(need, smem),
+                                          st));
   return AS_OK;
 }
 

@@ -181,9 +181,12 @@ def test_spmm_chunk_remainders_empty_rows(K, rng, k):
     assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("shape", [(200_000, 300_000, 3_000_000), (5_000, 2_000_000, 4_000_000)])
+@pytest.mark.parametrize("shape", [(200_000, 300_000, 3_000_000), (5_000, 2_000_000, 4_000_000),
+                                   (60_000, 40_000, 2_000_000)])
 def test_build_and_transpose_two_level_scatter(K, rng, shape):
-    # element data beyond L2: the two-level (super-bucket) scatter path
+    # element data beyond L2: the two-level (super-bucket) scatter path; the
+    # 2e6 case: CTA chunks above the shared-memory staging, below the
+    # two-level threshold (the direct per-element scatter)
     n_rows, n_cols, n = shape
     rows, cols = rng.integers(0, n_rows, n), rng.integers(0, n_cols, n)
     vals = rng.uniform(-1, 1, n)
