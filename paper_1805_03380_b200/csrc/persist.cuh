@@ -971,46 +971,47 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
     __syncthreads();
     for (long long b = tid; b < ncb; b += nthr) ha[b] = 0u;  // super-bucket cursors
   } else {
+    // staged scatter: the counts stay in ha for phase 2's local scan
+    const bool keep = a.stage != 0;
     for (long long b = tid; b < ncb; b += nthr) {
       const unsigned h = ha[b];
       hb[b] = h ? atomicAdd(&a.cb_cnt[b], h) : 0u;
+      if (!keep) ha[b] = 0u;
     }
-    if (a.stage) {  // local offsets of the staged scatter: scan of this CTA's counts
-      __syncthreads();
-      long long running = 0;
-      for (long long cb = 0; cb < ncb; cb += nthr) {
-        const long long b = cb + tid;
-        long long ctot;
-        const long long ex = block_exclusive_scan<long long>(b < ncb ? (long long)ha[b] : 0ll, xscan, &ctot);
-        if (b < ncb) hl[b] = (unsigned)(running + ex);
-        running += ctot;
-      }
-    }
-    __syncthreads();
-    for (long long b = tid; b < ncb; b += nthr) ha[b] = 0u;
   }
   grid_sync(a.gb, gen);
   AS_PHASE_MARK(a, gen);
 
   // ---------------- phase 2: every CTA scans the bucket counts ----------------
   {
+    // one scan of (this CTA's count << 32 | global count): the global bucket
+    // starts and, for the staged scatter, the CTA-local bucket offsets (the
+    // global total is < 2^31, so the low half never carries)
+    constexpr long long kLo = 0xffffffffll;
+    const bool staged = !kTwo && a.stage;
     long long running = 0;
     for (long long cb = 0; cb < ncb; cb += nthr) {
       const long long b = cb + tid;
-      const long long cnt = b < ncb ? (long long)__ldcg(&a.cb_cnt[b]) : 0;
+      long long cnt = b < ncb ? (long long)__ldcg(&a.cb_cnt[b]) : 0;
+      if (staged && b < ncb) {
+        cnt |= (long long)ha[b] << 32;
+        ha[b] = 0u;  // cursor of the scatter
+      }
       long long ctot;
       const long long ex = block_exclusive_scan<long long>(cnt, xscan, &ctot);
       if (b < ncb) {
+        const long long start = (running + ex) & kLo;
         if constexpr (kTwo) {
-          if (b % F == 0) hb[b / F] += (unsigned)(running + ex);  // super-bucket start
+          if (b % F == 0) hb[b / F] += (unsigned)start;  // super-bucket start
         } else {
-          hb[b] += (unsigned)(running + ex);  // slot base of this CTA's range
+          hb[b] += (unsigned)start;  // slot base of this CTA's range
+          if (staged) hl[b] = (unsigned)((running + ex) >> 32);
         }
-        if (g == 0) a.cb_start[b] = running + ex;
+        if (g == 0) a.cb_start[b] = start;
       }
       running += ctot;
     }
-    if (g == 0 && tid == 0) a.cb_start[ncb] = running;
+    if (g == 0 && tid == 0) a.cb_start[ncb] = running & kLo;
   }
   __syncthreads();
 
