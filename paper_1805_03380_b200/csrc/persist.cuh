@@ -265,7 +265,10 @@ struct NoSrc {
 #endif
 constexpr int kMaxCoarse = 8192;  // coarse buckets (two u32 arrays in smem)
 constexpr int kMaxW = 1024;       // columns per coarse bucket
-constexpr int kTBins = 1024;      // second-level bins per bucket tile
+#ifndef AS_TBINS
+#define AS_TBINS 1024
+#endif
+constexpr int kTBins = AS_TBINS;  // second-level bins per bucket tile
 
 template <class T, class S1, class S2>
 struct PersistArgs {
@@ -332,15 +335,15 @@ struct BTileSmem {
   } u;
   union {
     unsigned short excl[kCap + 8];
-    struct {
+    struct {  // the sort's bins and scatter (excl is written after it)
       unsigned cursor[kTBins];
       unsigned short bstart[kTBins + 8];
+      unsigned short perm2[kCap];
+      unsigned short sbin[kCap];
     } bk;
   } v;
   unsigned short scol[kCap];   // local column of each key (sk order)
   unsigned short perm[kCap];
-  unsigned short perm2[kCap];
-  unsigned short sbin[kCap];
   unsigned short cstart[kMaxW + 8];  // column boundaries (tile positions)
   unsigned hbits[kCap / 32];
   short med[kTBins], big[kTBins];
@@ -355,7 +358,10 @@ struct BTileSmem {
 
 // Dynamic shared memory of the persistent kernel: two CTAs per SM (the
 // register file is the binding limit), so ~110 KB each is free to use.
-constexpr int kPersistSmemBytes = 110 * 1024;
+#ifndef AS_PERSIST_SMEM_KB
+#define AS_PERSIST_SMEM_KB (AS_PERSIST_MINB == 1 ? 224 : 110)
+#endif
+constexpr int kPersistSmemBytes = AS_PERSIST_SMEM_KB * 1024;
 
 // Phases 1-3: colc, then three runtime-sized [n_cb] arrays (histogram /
 // cursor, the CTA's range inside each bucket, the CTA-local bucket offsets),
@@ -369,6 +375,7 @@ union PersistSmem {
   BTileSmem<T> t;
   unsigned char raw[kPersistSmemBytes];
 };
+static_assert(sizeof(BTileSmem<double>) <= kPersistSmemBytes, "tile above the shared-memory budget");
 
 // Scatter staging behind the [3 * n_cb] arrays: keys, values, columns of the
 // CTA's chunk in local bucket order.  Returns the capacity in elements.
@@ -616,8 +623,8 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int Wt, int row_bits) {
     const int b = bin_of(p);
     const unsigned slot = atomicAdd(&S.v.bk.cursor[b], 1u);
     S.u.sk2[slot] = S.sk[p];
-    S.perm2[slot] = S.perm[p];
-    S.sbin[slot] = (unsigned short)b;
+    S.v.bk.perm2[slot] = S.perm[p];
+    S.v.bk.sbin[slot] = (unsigned short)b;
   }
   if (tid == 0) {
     S.n_med = 0;
@@ -635,14 +642,14 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int Wt, int row_bits) {
     else if (L > kWarpSortMax) S.big[atomicAdd(&S.n_big, 1)] = (short)b;
   }
   for (int q = tid; q < m; q += nthr) {
-    const int b = S.sbin[q];
+    const int b = S.v.bk.sbin[q];
     const int s0 = S.v.bk.bstart[b], e0b = S.v.bk.bstart[b + 1];
     if (e0b - s0 <= kRankMax) {
       const unsigned long long k = S.u.sk2[q];
       int r = 0;
       for (int j = s0; j < e0b; j++) r += (S.u.sk2[j] < k);
       S.sk[s0 + r] = k;
-      S.perm[s0 + r] = S.perm2[q];
+      S.perm[s0 + r] = S.v.bk.perm2[q];
       S.scol[s0 + r] = col_of_bin(b);
     }
   }
@@ -652,20 +659,20 @@ __device__ void sort_bucket_smem(BTileSmem<T>& S, int m, int Wt, int row_bits) {
   for (int q = warp; q < n_med; q += nwarps) {
     const int b = S.med[q];
     const int s0 = S.v.bk.bstart[b], L = S.v.bk.bstart[b + 1] - s0;
-    bitonic_sort<false>(S.u.sk2 + s0, L, lane, 32, S.perm2 + s0);
+    bitonic_sort<false>(S.u.sk2 + s0, L, lane, 32, S.v.bk.perm2 + s0);
     for (int i = lane; i < L; i += 32) {
       S.sk[s0 + i] = S.u.sk2[s0 + i];
-      S.perm[s0 + i] = S.perm2[s0 + i];
+      S.perm[s0 + i] = S.v.bk.perm2[s0 + i];
       S.scol[s0 + i] = col_of_bin(b);
     }
   }
   for (int q = 0; q < n_big; q++) {
     const int b = S.big[q];
     const int s0 = S.v.bk.bstart[b], L = S.v.bk.bstart[b + 1] - s0;
-    bitonic_sort<true>(S.u.sk2 + s0, L, tid, nthr, S.perm2 + s0);
+    bitonic_sort<true>(S.u.sk2 + s0, L, tid, nthr, S.v.bk.perm2 + s0);
     for (int i = tid; i < L; i += nthr) {
       S.sk[s0 + i] = S.u.sk2[s0 + i];
-      S.perm[s0 + i] = S.perm2[s0 + i];
+      S.perm[s0 + i] = S.v.bk.perm2[s0 + i];
       S.scol[s0 + i] = col_of_bin(b);
     }
     __syncthreads();

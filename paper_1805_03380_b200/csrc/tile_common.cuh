@@ -16,7 +16,10 @@ namespace as {
 #define AS_SEG_THREADS 512
 #endif
 constexpr int kSegThreads = AS_SEG_THREADS;  // threads of a tile CTA
-constexpr int kCap = 2048;                  // elements of a shared-memory tile
+#ifndef AS_KCAP
+#define AS_KCAP 2048
+#endif
+constexpr int kCap = AS_KCAP;               // elements of a shared-memory tile
 constexpr int kItems = kCap / kSegThreads;  // 8 positions per thread
 constexpr int kWarpSortMax = 512;           // bins up to this sort in one warp
 constexpr int kRankMax = 32;                // bins up to this rank keys directly
