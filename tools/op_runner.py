@@ -1,6 +1,9 @@
 """Run one hot-path op a few times on its BASELINE config (for ncu captures).
 
-    python tools/op_runner.py build|flush|transpose|spmm|trace|add|spgemm [reps]
+    python tools/op_runner.py build|flush|transpose|spmm|trace|add|spgemm|all [reps]
+
+`all` runs every op in that order, `reps` times each, in one process (one
+ncu capture for the whole set).
 """
 import os
 import sys
@@ -15,6 +18,11 @@ from paper_1805_03380_b200 import _kernels, synth  # noqa: E402
 def main():
     op = sys.argv[1]
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    for o in (("build", "transpose", "flush", "spmm", "trace", "add", "spgemm") if op == "all" else (op,)):
+        run(o, reps)
+
+
+def run(op, reps):
     dev = torch.device("cuda")
 
     def T(a, dt):
