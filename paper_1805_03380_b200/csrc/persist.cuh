@@ -300,6 +300,7 @@ struct PersistArgs {
   GridBar gb;
   unsigned long long* phase_ts;  // optional: globaltimer after each phase (debug)
   int stage;                     // 1: phase 3 stages each CTA's chunk in shared memory (stage_layout)
+  long long dense_rows;          // pre mode: > 0 = output rows; columns above the tile take the dense path
   const long long* pre_ptr;      // non-null: input already bucketed by column (SpGEMM products)
   // bucket t spans columns [cb_col[t], cb_col[t+1]); pre_ptr mode: tiles are
   // taken in `order` (largest size class first)
@@ -832,6 +833,323 @@ __device__ long long process_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1
   return run_base;
 }
 
+// Pre-bucketed mode (SpGEMM): a tile of m <= kCap products [s, s+m) over Wt
+// columns sorted and folded in shared memory; kept entries to tmp[s + ...],
+// kept counts per column to col_kept.  Returns the tile's kept total.
+template <class T, class S1, class S2>
+__device__ long long pre_tile_to_tmp(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a, long long s, int m, unsigned col_base,
+                                     int Wt) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int i = tid; i < m; i += nthr) {
+    S.sk[i] = __ldcg(&a.keys[s + i]);
+    S.scol[i] = (unsigned short)(__ldcg(&a.colb[s + i]) - col_base);
+    S.perm[i] = (unsigned short)i;
+  }
+  __syncthreads();
+  sort_bucket_smem(S, m, Wt, a.row_bits);
+  bucket_chunk_reduce<T>(S, 0, m, m, nullptr, nullptr, col_base, a.vs, a.mode, a.prune, a.vals_b + s);
+  for (int p = tid; p < m; p += nthr) {
+    const unsigned e0 = S.v.excl[p], e1 = S.v.excl[p + 1];
+    if (e1 != e0) {
+      a.tmp_rows[s + e0] = (int)key_row(S.sk[p]);
+      a.tmp_vals[s + e0] = S.u.rv[p];
+    }
+  }
+  for (int l = tid; l < Wt; l += nthr) a.col_kept[col_base + l] = S.v.excl[S.cstart[l + 1]] - S.v.excl[S.cstart[l]];
+  const long long kept = S.v.excl[m];
+  __syncthreads();
+  return kept;
+}
+
+// Multi-product rows whose counters / list cursors live in shared memory
+// (more: global memory).
+constexpr int kDenseSmemCnt = 4096;
+
+// Shared memory of the dense column path for n_rows rows: two bitmaps of
+// nw = ceil(n_rows / 32) words, their u16 prefixes inside groups of 32 words
+// and the u32 group prefixes.
+__host__ __device__ inline long long dense_column_bytes(long long n_rows) {
+  const long long nw = (n_rows + 31) / 32;
+  return nw <= 0 ? 0 : 12 * nw + 8 * (nw / 32 + 2) + 16 + 4 * kDenseSmemCnt;
+}
+
+// One output column of SpGEMM with L products at [g0, g0 + L) (product
+// order = the reference's accumulation order: B entry, then A position),
+// folded without sorting the products (Gustavson's dense accumulator,
+// _kernels.py:83-93, made parallel):
+//   1. every product sets its row's bit in `seen`; a row seen before also
+//      sets `multi` (shared-memory bitmaps over all rows);
+//   2. coarse popcount prefixes: rank(row) = the row's position in the
+//      sorted output, mrank(row) = its index among the multi rows;
+//   3. a product of a single-product row is the output itself: written to
+//      tmp[out + rank]; a multi row counts its products;
+//   4. the multi rows' products are listed per row (scan of the counts,
+//      then placement) and each multi row folds its few products in product
+//      order (first assigns, then +=: kSumSeq), written to tmp[out + rank];
+//   5. exact zeros (underflowed products, cancellations) are compacted away.
+// Scratch: keys_alt / colb_alt at [g0, g0 + L) (free in pre mode).  Returns
+// the kept count.
+template <class T, class S1, class S2>
+__device__ long long pre_dense_column(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a, long long g0, long long L,
+                                      long long out) {
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+  const int nw = (int)((a.dense_rows + 31) / 32);  // bitmap words
+  const int ng = (nw + 31) >> 5;                  // groups of 32 words
+  unsigned* seen = reinterpret_cast<unsigned*>(&S);
+  unsigned* multi = seen + nw;
+  unsigned* sgrp = multi + nw;   // [ng + 1] seen prefix per group
+  unsigned* mgrp = sgrp + ng + 1;  // [ng + 1] multi prefix per group
+  unsigned short* spre = reinterpret_cast<unsigned short*>(mgrp + ng + 1);  // [nw] seen prefix inside the group
+  unsigned short* mpre = spre + nw;                                          // [nw] multi prefix inside the group
+  unsigned* scnt = reinterpret_cast<unsigned*>(reinterpret_cast<unsigned char*>(seen) +
+                                               ((dense_column_bytes(a.dense_rows) - 4 * kDenseSmemCnt) & ~15ll));
+  __shared__ unsigned s_tot[2];
+  __shared__ int s_zero;
+  __shared__ long long s_scan[kSegThreads / 32 + 1];  // the tile's scan_tmp lies under the bitmaps
+  for (int w = tid; w < 2 * nw; w += nthr) seen[w] = 0u;
+  if (tid == 0) s_zero = 0;
+  __syncthreads();
+  tt_mark(12);
+  const unsigned long long* gk = a.keys + g0;
+  // 1. seen / multi
+  constexpr int kU = 8;  // products in flight per thread (the keys stream from HBM)
+  for (long long i0 = tid; i0 < L; i0 += (long long)kU * nthr) {
+    unsigned r[kU];
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      const long long i = i0 + (long long)u * nthr;
+      r[u] = i < L ? key_row(__ldcg(&gk[i])) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      if (r[u] == 0xffffffffu) continue;
+      const unsigned bit = 1u << (r[u] & 31);
+      if (atomicOr(&seen[r[u] >> 5], bit) & bit) atomicOr(&multi[r[u] >> 5], bit);
+    }
+  }
+  __syncthreads();
+  tt_mark(13);
+  // 2. prefixes: per word inside its group of 32 (one warp per group), then
+  //    over the groups (both counts in one scan: multi << 32 | seen)
+  for (int g = warp; g < ng; g += nwarps) {
+    const int w = g * 32 + lane;
+    const unsigned cs = w < nw ? __popc(seen[w]) : 0u, cm = w < nw ? __popc(multi[w]) : 0u;
+    const unsigned is = warp_inclusive_scan(cs), im = warp_inclusive_scan(cm);
+    if (w < nw) {
+      spre[w] = (unsigned short)(is - cs);
+      mpre[w] = (unsigned short)(im - cm);
+    }
+    if (lane == 31) {
+      sgrp[g] = is;
+      mgrp[g] = im;
+    }
+  }
+  __syncthreads();
+  {
+    unsigned long long run = 0;
+    for (int g0g = 0; g0g < ng; g0g += nthr) {
+      const int g = g0g + tid;
+      const unsigned long long c = g < ng ? (((unsigned long long)mgrp[g] << 32) | sgrp[g]) : 0ull;
+      long long tot;
+      const long long ex = block_exclusive_scan<long long>((long long)c, s_scan, &tot);
+      if (g < ng) {
+        sgrp[g] = (unsigned)((run + ex) & 0xffffffffull);
+        mgrp[g] = (unsigned)((run + ex) >> 32);
+      }
+      run += (unsigned long long)tot;
+    }
+    if (tid == 0) {
+      s_tot[0] = (unsigned)(run & 0xffffffffull);
+      s_tot[1] = (unsigned)(run >> 32);
+    }
+  }
+  __syncthreads();
+  tt_mark(14);
+  const unsigned touched = s_tot[0], n_mr = s_tot[1];
+  // the output rows in order straight from the bitmap (coalesced; the values
+  // below land at the same ranks)
+  for (int w = tid; w < nw; w += nthr) {
+    unsigned bits = seen[w];
+    unsigned rk = sgrp[w >> 5] + spre[w];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1u;
+      a.tmp_rows[out + rk++] = w * 32 + b;
+    }
+  }
+  auto rank_in = [&](const unsigned* bm, const unsigned* grp, const unsigned short* pre, unsigned r) -> unsigned {
+    const int w = (int)(r >> 5);
+    return grp[w >> 5] + pre[w] + __popc(bm[w] & ((1u << (r & 31)) - 1u));
+  };
+  unsigned long long* meta = a.keys_alt + g0;                              // [n_mr] (rank << 32) | row
+  unsigned* cnt = n_mr <= (unsigned)kDenseSmemCnt
+                      ? scnt
+                      : reinterpret_cast<unsigned*>(a.keys_alt + g0 + (L + 1) / 2);  // [n_mr] counts, then cursors
+  unsigned* list = a.colb_alt + g0;                                         // [multi products] local index
+  unsigned* mlist = a.colb + g0;  // [multi products] their local indices (colb is free here)
+  __shared__ unsigned s_nmp;
+  for (unsigned q = tid; q < n_mr; q += nthr) cnt[q] = 0u;
+  if (tid == 0) s_nmp = 0u;
+  __syncthreads();
+  // 3. single-product rows straight to their output slot; multi rows count
+  const T* gv = reinterpret_cast<const T*>(a.vals_b) + g0;
+  bool zero = false;
+  constexpr int kU3 = 4;
+  for (long long i0 = tid; i0 < L; i0 += (long long)kU3 * nthr) {  // warp-uniform trip count
+    unsigned r[kU3];
+    T v[kU3];
+#pragma unroll
+    for (int u = 0; u < kU3; u++) {
+      const long long i = i0 + (long long)u * nthr;
+      r[u] = 0xffffffffu;
+      if (i < L) {
+        r[u] = key_row(__ldcg(&gk[i]));
+        v[u] = __ldcg(&gv[i]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU3; u++) {
+      bool is_multi = false;
+      if (r[u] != 0xffffffffu) {
+        const unsigned bit = 1u << (r[u] & 31);
+        const unsigned rk = rank_in(seen, sgrp, spre, r[u]);
+        if (!(multi[r[u] >> 5] & bit)) {
+          a.tmp_vals[out + rk] = v[u];  // (the rows come from the bitmap, below)
+          zero |= (v[u] == T(0));
+        } else {
+          const unsigned mr = rank_in(multi, mgrp, mpre, r[u]);
+          atomicAdd(&cnt[mr], 1u);
+          meta[mr] = ((unsigned long long)rk << 32) | r[u];
+          is_multi = true;
+        }
+      }
+      // warp-aggregated append of the multi products
+      const unsigned ball = __ballot_sync(__activemask(), is_multi);
+      unsigned base = 0;
+      if ((tid & 31) == __ffs(ball | 0x80000000u) - 1 && ball) base = atomicAdd(&s_nmp, (unsigned)__popc(ball));
+      base = __shfl_sync(__activemask(), base, __ffs(ball | 0x80000000u) - 1);
+      if (is_multi) mlist[base + __popc(ball & lanemask_lt())] = (unsigned)(i0 + (long long)u * nthr);
+    }
+  }
+  __syncthreads();
+  tt_mark(15);
+  // 4. per multi row: its segment of the list (exclusive scan of the counts)
+  {
+    long long run = 0;
+    for (unsigned q0 = 0; q0 < n_mr; q0 += nthr) {
+      const unsigned q = q0 + tid;
+      const long long c = q < n_mr ? (long long)cnt[q] : 0ll;
+      long long tot;
+      const long long ex = block_exclusive_scan<long long>(c, s_scan, &tot);
+      if (q < n_mr) cnt[q] = (unsigned)(run + ex);
+      run += tot;
+    }
+  }
+  __syncthreads();
+  tt_mark(16);
+  if (n_mr > 0) {
+    const unsigned nmp = s_nmp;  // only the multi products, listed by the pass above
+    for (unsigned j0 = tid; j0 < nmp; j0 += 4u * nthr) {
+      unsigned ii[4], r[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) ii[u] = j0 + u * nthr < nmp ? __ldcg(&mlist[j0 + u * nthr]) : 0xffffffffu;
+#pragma unroll
+      for (int u = 0; u < 4; u++) r[u] = ii[u] != 0xffffffffu ? key_row(__ldcg(&gk[ii[u]])) : 0u;
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (ii[u] != 0xffffffffu) list[atomicAdd(&cnt[rank_in(multi, mgrp, mpre, r[u])], 1u)] = ii[u];
+    }
+    __syncthreads();
+    tt_mark(19);
+    for (unsigned q = tid; q < n_mr; q += nthr) {
+      const unsigned st = q ? cnt[q - 1] : 0u, en = cnt[q];
+      T acc;
+      if (en - st <= 8) {  // the row's products in product order: sorted in registers
+        unsigned li[8];
+#pragma unroll
+        for (int x = 0; x < 8; x++) li[x] = st + x < en ? list[st + x] : 0xffffffffu;
+#pragma unroll
+        for (int x = 1; x < 8; x++)
+#pragma unroll
+          for (int y = x; y > 0; y--)
+            if (li[y] < li[y - 1]) {
+              const unsigned t2 = li[y];
+              li[y] = li[y - 1];
+              li[y - 1] = t2;
+            }
+        T vv[8];
+#pragma unroll
+        for (int x = 0; x < 8; x++) vv[x] = li[x] != 0xffffffffu ? __ldcg(&gv[li[x]]) : T(0);
+        acc = vv[0];
+#pragma unroll
+        for (int x = 1; x < 8; x++)
+          if (li[x] != 0xffffffffu) acc = acc + vv[x];
+      } else {  // long: insertion sort in place
+        for (unsigned x = st + 1; x < en; x++) {
+          const unsigned key = list[x];
+          unsigned y = x;
+          while (y > st && list[y - 1] > key) {
+            list[y] = list[y - 1];
+            y--;
+          }
+          list[y] = key;
+        }
+        acc = __ldcg(&gv[list[st]]);
+        for (unsigned x = st + 1; x < en; x++) acc = acc + __ldcg(&gv[list[x]]);
+      }
+      const unsigned long long mt = meta[q];
+      a.tmp_vals[out + (mt >> 32)] = acc;
+      zero |= (acc == T(0));
+    }
+  }
+  if (zero) s_zero = 1;
+  __syncthreads();
+  tt_mark(17);
+  if (!s_zero || !a.prune) return touched;
+  // 5. compact the exact zeros away (rare), chunk by chunk in place
+  long long w = 0;
+  for (long long b = 0; b < touched; b += nthr) {
+    const long long i = b + tid;
+    int r = 0;
+    T v = T(0);
+    if (i < touched) {
+      r = __ldcg(&a.tmp_rows[out + i]);
+      v = __ldcg(&a.tmp_vals[out + i]);
+    }
+    const bool keep = i < touched && v != T(0);
+    long long tot;
+    const long long ex = block_exclusive_scan<long long>(keep ? 1ll : 0ll, s_scan, &tot);
+    if (keep) {
+      a.tmp_rows[out + w + ex] = r;
+      a.tmp_vals[out + w + ex] = v;
+    }
+    w += tot;
+    __syncthreads();
+  }
+  return w;
+}
+
+// Pre mode, a bucket above the tile: all its columns but the last hold at
+// most kPreT products (the bucket rule), so they are one shared-memory tile;
+// the last column goes through the dense column path.
+template <class T, class S1, class S2>
+__device__ void pre_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a, long long s, long long m,
+                                     unsigned col_base, int Wt) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const unsigned c_last = col_base + (unsigned)Wt - 1u;
+  const long long mp = __ldg(&a.pre_ptr[c_last]) - s;
+  long long kept_p = 0;
+  if (mp > 0) {
+    kept_p = pre_tile_to_tmp<T>(S, a, s, (int)mp, col_base, Wt - 1);
+  } else {
+    for (int l = tid; l < Wt - 1; l += nthr) a.col_kept[col_base + l] = 0u;
+  }
+  tt_mark(18);
+  const long long kh = pre_dense_column<T>(S, a, s + mp, m - mp, s + kept_p);
+  if (tid == 0) a.col_kept[c_last] = (unsigned)kh;
+  __syncthreads();
+}
+
 // Executed by one full warp of the tile: the exclusive prefix of bucket t's
 // kept count over buckets [0, t).  Each bucket publishes its count to st[t]
 // and adds it to its group word grp[t / 32] (publishers << 56 | sum); the
@@ -897,6 +1215,7 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
   a.s1.set_cache(SM.h.colc);
   a.s2.set_cache(SM.h.colc);
 
+  long long n_work = ncb;  // pre mode: buckets with columns (the rest are skipped)
   if constexpr (kPre) {
     // pre-bucketed input (SpGEMM products): keys / colb / vals_b already sit
     // in output-column order; only the coarse bucket starts are needed
@@ -922,9 +1241,11 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
         a.cb_col[ncb] = (unsigned)a.n_cols;
         a.cb_start[ncb] = __ldg(&a.pre_ptr[a.n_cols]);
       }
-      // size class (largest first: a rough longest-processing-time order)
+      // size class (largest first: a rough longest-processing-time order);
+      // class 4 = no columns at all (targets inside one long column): never
+      // handed out
       const long long mt = __ldg(&a.pre_ptr[c1]) - s0;
-      const unsigned cls = mt > 32 * kCap ? 0u : mt > 4 * kCap ? 1u : mt > kCap ? 2u : 3u;
+      const unsigned cls = c1 == c0 ? 4u : mt > 32 * kCap ? 0u : mt > 4 * kCap ? 1u : mt > kCap ? 2u : 3u;
       const unsigned peers = __match_any_sync(__activemask(), cls);  // warp-aggregated slot
       const int leader = __ffs(peers) - 1;
       unsigned slot0 = 0;
@@ -934,12 +1255,13 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
     }
     grid_sync(a.gb, gen);
     {
-      unsigned base[4];
+      unsigned base[5];
       base[0] = 0;
-      for (int q = 1; q < 4; q++) base[q] = base[q - 1] + __ldcg(a.ticket + q);
+      for (int q = 1; q < 5; q++) base[q] = base[q - 1] + __ldcg(a.ticket + q);
+      n_work = base[4];
       for (long long t = g * nthr + tid; t < ncb; t += G * nthr) {
         const unsigned v = __ldcg(&a.cb_cnt[t]);
-        a.order[base[v >> 28] + (v & 0x0fffffffu)] = (unsigned)t;
+        if ((v >> 28) < 4u) a.order[base[v >> 28] + (v & 0x0fffffffu)] = (unsigned)t;
       }
     }
     grid_sync(a.gb, gen);
@@ -1156,7 +1478,7 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
   while (true) {
     if (tid == 0) {
       long long t = (long long)atomicAdd(a.ticket, 1u);
-      if (t < ncb && a.order) t = __ldcg(&a.order[t]);
+      if (a.order) t = t < n_work ? (long long)__ldcg(&a.order[t]) : ncb;
       S.tile = t;
       if (t < ncb) {
         S.s = __ldcg(&a.cb_start[t]);
@@ -1245,6 +1567,8 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
         }
         for (int l = tid; l < Wt; l += nthr) a.col_ptr[col_base + l] = (int)(base + S.v.excl[S.cstart[l]]);
       }
+    } else if (kPre && a.dense_rows > 0) {
+      if constexpr (kPre) pre_oversized_bucket<T>(S, a, s, m, col_base, Wt);
     } else {
       const long long kept = process_oversized_bucket<T>(S, a, s, m, col_base, Wt);
       if constexpr (!kPre) {

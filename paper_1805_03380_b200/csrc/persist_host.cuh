@@ -13,6 +13,7 @@ constexpr long long kMaxDim = 0x7fffffffll;
 constexpr long long kMaxGrid = 148 * 8;  // upper bound of the co-resident grid
 
 struct PersistWs {
+  long long dense_rows = 0;  // pre mode: rows of the output (dense column path when they fit)
   unsigned* zero;  // [0] ticket, [16] barrier arrive, [32] barrier generation, then cb_cnt
   unsigned* cb_cnt;
   size_t zero_bytes;
@@ -143,7 +144,7 @@ static int launch_persist_k(PersistArgs<T, S1, S2>& a, cudaStream_t st) {
   // rest of the 256 KB goes back to L1 (the pre-bucketed SpGEMM tiles gather
   // through it)
   constexpr bool kPre = std::is_same<S1, NoSrc<T>>::value && std::is_same<S2, NoSrc<T>>::value;
-  const size_t need = kPre ? sizeof(BTileSmem<T>)
+  const size_t need = kPre ? std::max(sizeof(BTileSmem<T>), (size_t)(a.dense_rows ? dense_column_bytes(a.dense_rows) : 0))
                       : a.stage ? smem
                                 : std::max(sizeof(BTileSmem<T>),
                                            (size_t)(((long long)sizeof(int) * (kColCache + 1) + 12ll * a.n_cb + 15) & ~15ll));
@@ -213,6 +214,7 @@ static int run_persist_ws(PersistWs& w, const S1& s1, const S2& s2, long long n,
   a.sb_cnt = w.sb_cnt;
   a.sb_fill = w.sb_fill;
   a.vals_alt = (T*)w.vals_alt;
+  a.dense_rows = (pre_ptr && dense_column_bytes(w.dense_rows) <= (long long)kPersistSmemBytes) ? w.dense_rows : 0;
   static unsigned long long* dbg_ts = nullptr;
   const bool phase_dbg = getenv("AS_PHASE_TIMES") != nullptr;
   if (phase_dbg) {
@@ -241,7 +243,7 @@ static int run_persist_ws(PersistWs& w, const S1& s1, const S2& s2, long long n,
     AS_CUDA_TRY(cudaMemcpyFromSymbolAsync(tt, g_tt, sizeof(tt), 0, cudaMemcpyDeviceToHost, st));
     AS_CUDA_TRY(cudaStreamSynchronize(st));
     fprintf(stderr, "[tile steps, block 0, kcycles]");
-    for (int i = 0; i < 12; i++) fprintf(stderr, " %d:%.1f", i, tt[i] * 1e-3);
+    for (int i = 0; i < 20; i++) fprintf(stderr, " %d:%.1f", i, tt[i] * 1e-3);
     fprintf(stderr, "\n");
 #endif
   }

@@ -261,6 +261,7 @@ int as_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int
   unsigned long long* states;
   long long *ent_ptr, *bounds;
   carve_spgemm(c, &w, n_cols_b, nnz_b, total_products, &scan_zero, &zb, &states, &lens, &ent_ptr, &bounds);
+  w.dense_rows = n_rows_a;
   AS_REQUIRE(c.ok, AS_ERR_ARG, "workspace too small: %zu < %zu", ws_bytes, c.off);
   if (n_cols_b > 0 && nnz_b > 0 && total_products > 0) {
     const long long per = (long long)kScanThreads * kScanItems;
