@@ -887,8 +887,8 @@ __host__ __device__ inline long long dense_column_bytes(long long n_rows) {
 //      then placement) and each multi row folds its few products in product
 //      order (first assigns, then +=: kSumSeq), written to tmp[out + rank];
 //   5. exact zeros (underflowed products, cancellations) are compacted away.
-// Scratch: keys_alt / colb_alt at [g0, g0 + L) (free in pre mode).  Returns
-// the kept count.
+// Scratch: keys_alt / colb_alt (and the keys of a row-only column) at
+// [g0, g0 + L) (free in pre mode).  Returns the kept count.
 template <class T, class S1, class S2>
 __device__ long long pre_dense_column(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a, long long g0, long long L,
                                       long long out) {
@@ -910,7 +910,12 @@ __device__ long long pre_dense_column(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a
   if (tid == 0) s_zero = 0;
   __syncthreads();
   tt_mark(12);
+  // rows of the products: a column above kCap products was expanded without
+  // keys, its rows in colb (spgemm_expand_kernel); a smaller one has keys
+  const bool rows_in_colb = L > kCap;
+  const unsigned* grow = a.colb + g0;
   const unsigned long long* gk = a.keys + g0;
+  auto row_at = [&](long long i) -> unsigned { return rows_in_colb ? __ldcg(&grow[i]) : key_row(__ldcg(&gk[i])); };
   // 1. seen / multi
   constexpr int kU = 8;  // products in flight per thread (the keys stream from HBM)
   for (long long i0 = tid; i0 < L; i0 += (long long)kU * nthr) {
@@ -918,7 +923,7 @@ __device__ long long pre_dense_column(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a
 #pragma unroll
     for (int u = 0; u < kU; u++) {
       const long long i = i0 + (long long)u * nthr;
-      r[u] = i < L ? key_row(__ldcg(&gk[i])) : 0xffffffffu;
+      r[u] = i < L ? row_at(i) : 0xffffffffu;
     }
 #pragma unroll
     for (int u = 0; u < kU; u++) {
@@ -986,7 +991,10 @@ __device__ long long pre_dense_column(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a
                       ? scnt
                       : reinterpret_cast<unsigned*>(a.keys_alt + g0 + (L + 1) / 2);  // [n_mr] counts, then cursors
   unsigned* list = a.colb_alt + g0;                                         // [multi products] local index
-  unsigned* mlist = a.colb + g0;  // [multi products] their local indices (colb is free here)
+  // [multi products] local indices: in the unused keys of a row-only column,
+  // else behind meta (n_mr <= kDenseSmemCnt then: the counts are in shared memory)
+  unsigned* mlist = rows_in_colb ? reinterpret_cast<unsigned*>(a.keys + g0)
+                                 : reinterpret_cast<unsigned*>(a.keys_alt + g0 + (L + 1) / 2);
   __shared__ unsigned s_nmp;
   for (unsigned q = tid; q < n_mr; q += nthr) cnt[q] = 0u;
   if (tid == 0) s_nmp = 0u;
@@ -1003,7 +1011,7 @@ __device__ long long pre_dense_column(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a
       const long long i = i0 + (long long)u * nthr;
       r[u] = 0xffffffffu;
       if (i < L) {
-        r[u] = key_row(__ldcg(&gk[i]));
+        r[u] = row_at(i);
         v[u] = __ldcg(&gv[i]);
       }
     }
@@ -1054,7 +1062,7 @@ __device__ long long pre_dense_column(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a
 #pragma unroll
       for (int u = 0; u < 4; u++) ii[u] = j0 + u * nthr < nmp ? __ldcg(&mlist[j0 + u * nthr]) : 0xffffffffu;
 #pragma unroll
-      for (int u = 0; u < 4; u++) r[u] = ii[u] != 0xffffffffu ? key_row(__ldcg(&gk[ii[u]])) : 0u;
+      for (int u = 0; u < 4; u++) r[u] = ii[u] != 0xffffffffu ? row_at(ii[u]) : 0u;
 #pragma unroll
       for (int u = 0; u < 4; u++)
         if (ii[u] != 0xffffffffu) list[atomicAdd(&cnt[rank_in(multi, mgrp, mpre, r[u])], 1u)] = ii[u];

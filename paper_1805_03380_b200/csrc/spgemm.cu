@@ -104,8 +104,12 @@ spgemm_expand_kernel(long long nnz_b, long long n_cols_b, long long total, const
                      const int* __restrict__ a_rows, const double* __restrict__ a_vals,
                      const int* __restrict__ b_ptr, const int* __restrict__ b_rows,
                      const double* __restrict__ b_vals, const long long* __restrict__ ent_ptr,
-                     const long long* __restrict__ bounds, unsigned long long* __restrict__ keys,
-                     unsigned* __restrict__ colb, double* __restrict__ pvals) {
+                     const long long* __restrict__ bounds, const long long* __restrict__ prod_ptr,
+                     long long dense_min, unsigned long long* __restrict__ keys, unsigned* __restrict__ colb,
+                     double* __restrict__ pvals) {
+  // products of a column with more than dense_min products go to the dense
+  // column path of the bucket kernel, which needs only their row (in colb)
+  // and value: no key, no column
   __shared__ int s_off[kExWin];  // ent_ptr[kk] - P0 (clamped below at 0 for the first entry)
   __shared__ int s_ast[kExWin];  // A column start of the entry, shifted to the entry's product 0
   __shared__ int s_col[kExWin];
@@ -118,6 +122,7 @@ spgemm_expand_kernel(long long nnz_b, long long n_cols_b, long long total, const
     const long long j0 = __ldg(&bounds[4 * t + 2]), j1 = __ldg(&bounds[4 * t + 3]);
     const int nw = (int)(kk1 - kk0 + 1);
     const bool staged = nw <= kExWin;
+    auto dense_col = [&](long long c) { return __ldg(&prod_ptr[c + 1]) - __ldg(&prod_ptr[c]) > dense_min; };
     if (staged) {
       for (int e = tid; e < nw; e += kExThreads) {
         const long long kk = kk0 + e;
@@ -133,7 +138,7 @@ spgemm_expand_kernel(long long nnz_b, long long n_cols_b, long long total, const
           if (__ldg(&b_ptr[mid]) <= kk) lo = mid;
           else hi = mid - 1;
         }
-        s_col[e] = (int)lo;
+        s_col[e] = dense_col(lo) ? -1 - (int)lo : (int)lo;  // negative: dense column
       }
       __syncthreads();
     }
@@ -171,8 +176,14 @@ spgemm_expand_kernel(long long nnz_b, long long n_cols_b, long long total, const
         col = (int)cl;
       }
       const long long pos = P0 + q;
-      keys[pos] = ((unsigned long long)(unsigned)__ldg(&a_rows[ii]) << 32) | (unsigned long long)pos;
-      colb[pos] = (unsigned)col;
+      const unsigned row = (unsigned)__ldg(&a_rows[ii]);
+      if (!staged && dense_col(col)) col = -1 - col;
+      if (col >= 0) {
+        keys[pos] = ((unsigned long long)row << 32) | (unsigned long long)pos;
+        colb[pos] = (unsigned)col;
+      } else {
+        colb[pos] = row;
+      }
       pvals[pos] = __dmul_rn(__ldg(&a_vals[ii]), bv);
     }
   }
@@ -262,6 +273,9 @@ int as_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int
   long long *ent_ptr, *bounds;
   carve_spgemm(c, &w, n_cols_b, nnz_b, total_products, &scan_zero, &zb, &states, &lens, &ent_ptr, &bounds);
   w.dense_rows = n_rows_a;
+  // the dense column path (and the expand's row-only products) when the
+  // output rows fit its shared-memory bitmaps
+  const bool dense = dense_column_bytes(n_rows_a) <= (long long)kPersistSmemBytes;
   AS_REQUIRE(c.ok, AS_ERR_ARG, "workspace too small: %zu < %zu", ws_bytes, c.off);
   if (n_cols_b > 0 && nnz_b > 0 && total_products > 0) {
     const long long per = (long long)kScanThreads * kScanItems;
@@ -277,7 +291,7 @@ int as_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int
     AS_LAUNCH_CHECK();
     spgemm_expand_kernel<<<(unsigned)std::min<long long>(ranges, (long long)kNumSMs * 32), kExThreads, 0, st>>>(
         nnz_b, n_cols_b, total_products, a_col_ptr, a_row_idx, a_vals, b_col_ptr, b_row_idx, b_vals, ent_ptr, bounds,
-        w.keys, w.colb, (double*)w.vals_b);
+        (const long long*)prod_ptr, dense ? (long long)kCap : LLONG_MAX, w.keys, w.colb, (double*)w.vals_b);
     AS_LAUNCH_CHECK();
   }
   ValSrc<double> vs{(const double*)w.vals_b, nullptr, (unsigned long long)total_products};

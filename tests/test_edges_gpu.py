@@ -195,3 +195,44 @@ def test_build_and_transpose_two_level_scatter(K, rng, shape):
     assert_csc_equal(got, want, exact_values=True)
     t = K.transpose(n_rows, n_cols, *_csc(want))
     assert_csc_equal(_np(t), oracle.transpose(n_rows, n_cols, *want), exact_values=True)
+
+
+@pytest.mark.parametrize("heavy", [1500, 2047, 2049, 20000])
+def test_spgemm_dense_column_path_boundaries(K, rng, heavy):
+    # light columns then one column of `heavy` products in the same
+    # pre-bucketed bucket: the bucket is above the tile, its last column
+    # takes the dense path -- with keys (<= 2048 products) or row-only
+    # products (> 2048); collisions from two A columns hitting the same rows
+    m = 30_000
+    a_rows = [rng.choice(m, heavy, replace=False), rng.choice(m, heavy // 2, replace=False)]
+    a_cols = [np.zeros(heavy, np.int64), np.ones(heavy // 2, np.int64)]
+    a_rows.append(rng.integers(0, m, 2000))
+    a_cols.append(rng.integers(2, 1000, 2000))
+    ar, ac = np.concatenate(a_rows), np.concatenate(a_cols)
+    a = oracle.canonicalize(m, 1000, ar, ac, rng.standard_normal(ar.shape[0]))
+    n = 800
+    b_rows = [rng.integers(2, 1000, 768), np.array([0, 1])]
+    b_cols = [np.repeat(np.arange(384), 2), np.array([384, 384])]
+    b_rows.append(rng.integers(0, 1000, 600))
+    b_cols.append(rng.integers(385, n, 600))
+    br, bc = np.concatenate(b_rows), np.concatenate(b_cols)
+    bv = rng.standard_normal(br.shape[0])
+    bv[-5:] = 0.0  # explicit zeros dropped by canonicalize
+    b = oracle.canonicalize(1000, n, br, bc, bv)
+    got = K.spgemm(m, 1000, n, _csc(a), _csc(b))
+    assert_csc_equal(_np(got), oracle.spgemm(m, *a, *b, n), exact_values=True)
+
+
+def test_spgemm_dense_column_cancellation_and_underflow(K):
+    # exact cancellations and underflowing products inside a dense column are
+    # pruned like the reference's `!= 0.0` filter
+    m = 5000
+    rows0 = np.arange(3000)
+    a = oracle.canonicalize(m, 3, np.concatenate([rows0, rows0, rows0[:10]]),
+                            np.concatenate([np.zeros(3000, np.int64), np.ones(3000, np.int64), np.full(10, 2)]),
+                            np.concatenate([np.full(3000, 1.5), np.full(3000, -1.5), np.full(10, 1e-300)]))
+    b = oracle.canonicalize(3, 2, np.array([0, 1, 2, 0]), np.array([0, 0, 0, 1]), np.array([2.0, 2.0, 1e-300, 1.0]))
+    got = K.spgemm(m, 3, 2, _csc(a), _csc(b))
+    want = oracle.spgemm(m, *a, *b, 2)
+    assert_csc_equal(_np(got), want, exact_values=True)
+    assert int(want[2][1]) == 0  # column 0 cancels / underflows to nothing
