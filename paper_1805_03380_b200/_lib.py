@@ -16,7 +16,7 @@ import torch
 from .errors import CoordinateError, CorruptionError, ShapeError, SparseError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbsparse.so")
+LIB_PATH = os.environ.get("AS_LIB_PATH") or os.path.join(_HERE, "libbsparse.so")  # override: build-variant experiments
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64

@@ -6,85 +6,134 @@
 // rounded, as numba evaluates it: no FMA), others alpha*a or beta*b; exact
 // zeros are pruned.
 //
-// B200 design: one cooperative launch of the co-resident grid.  The (A,B)
-// column pairs form one merged sequence (merge.cuh); each CTA owns a
-// contiguous range and walks it in chunks, each thread merging kAddItems
-// consecutive positions.  Pass 1 counts the surviving entries, a grid
-// barrier and a grid-wide prefix over the CTA totals give every CTA its
-// output offset, pass 2 re-merges, stages the compacted chunk in shared
-// memory and writes it with coalesced stores; the thread owning a column's
-// first merged position writes its col_ptr.  No per-tile look-back chain.
+// B200 design: a canonical CSC is sorted by the composite key (column, row),
+// so the whole add is ONE merge of two sorted sequences (A wins ties; a
+// coincident pair occupies two merged positions, the A one emits the sum and
+// the B one emits nothing).  Merged positions are cut into tiles of kAddTile:
+//  1. add_partition_kernel, one thread per column: every tile boundary that
+//     falls inside the column gets its merge-path split (global A / B element
+//     index), the column holding it and a flag telling whether the tile's
+//     first B element pairs with the A element just before the tile; the
+//     column holding each tile's last position is recorded too;
+//  2. add_tile_kernel, persistent CTAs taking tiles in ticket order: the tile's A and B
+//     ranges are contiguous in the inputs, loaded coalesced into shared
+//     memory; each element's column comes from a block max-scan of the
+//     column starts, giving 64-bit composite keys; each thread merge-path
+//     splits its kAddItems positions in shared memory and merges them; a
+//     block scan of kept counts and a single-pass decoupled look-back give
+//     the output offset; rows / values go out through shared memory
+//     (coalesced) and the tile writes col_ptr of the columns whose merged
+//     start lies in it.
+// One pass over the data, no grid barrier, no re-merge.
 #include "capi_util.cuh"
 #include "common.cuh"
-#include "merge.cuh"
 
 namespace as {
 
-constexpr int kAddItems = 8;
-constexpr int kAddChunk = kMThreads * kAddItems;
+#ifndef AS_ADD_THREADS
+#define AS_ADD_THREADS 256
+#endif
+#ifndef AS_ADD_ITEMS
+#define AS_ADD_ITEMS 8
+#endif
+#ifndef AS_ADD_MINB
+#define AS_ADD_MINB 4
+#endif
+constexpr int kAddThreads = AS_ADD_THREADS;
+constexpr int kAddItems = AS_ADD_ITEMS;
+constexpr int kAddTile = kAddThreads * kAddItems;
+constexpr int kAddPartThreads = 256;
 
-// Merge positions [d0, d1) starting in column c.  emit(row, value) for kept
-// outputs in order; on_col(c, produced) for every column whose start this
-// thread owns (including empty columns sharing the position).
-template <class Emit, class OnCol>
-__device__ void merge_range(long long n_cols, long long c, long long d0, long long d1, const int* __restrict__ ap,
-                            const int* __restrict__ ar, const double* __restrict__ av, const int* __restrict__ bp,
-                            const int* __restrict__ br, const double* __restrict__ bv, double alpha, double beta,
-                            Emit emit, OnCol on_col) {
-  long long a0 = __ldg(&ap[c]), b0 = __ldg(&bp[c]);
-  long long la = __ldg(&ap[c + 1]) - a0, lb = __ldg(&bp[c + 1]) - b0;
-  const long long dl = d0 - (a0 + b0);
-  if (dl == 0)  // we own the starts of c and of the empty columns before it sharing the position
-    for (long long cc = c; cc >= 0 && mstart_of(ap, bp, cc) == d0; cc--) on_col(cc, 0);
-  long long i, j;
-  split_at(ar, br, a0, b0, la, lb, dl, &i, &j);
-  long long pos = a0 + b0 + i + j;
-  int produced = 0;
-  while (pos < d1) {
-    if (i == la && j == lb) {
-      c++;
-      a0 = __ldg(&ap[c]);
-      b0 = __ldg(&bp[c]);
-      la = __ldg(&ap[c + 1]) - a0;
-      lb = __ldg(&bp[c + 1]) - b0;
-      i = j = 0;
-      on_col(c, produced);
-      continue;
+struct AddDesc {
+  int ia;    // first A element of the tile
+  int jb;    // first B element of the tile
+  int skip;  // B[jb] coincides with A[ia - 1] (its sum was emitted by the previous tile)
+  int col;   // column holding the tile's first merged position
+};
+
+// One thread per column: tile boundaries inside it.
+__global__ void __launch_bounds__(kAddPartThreads)
+add_partition_kernel(long long n_cols, long long nnz_a, long long nnz_b, long long n_tiles, const int* __restrict__ ap,
+                     const int* __restrict__ ar, const int* __restrict__ bp, const int* __restrict__ br,
+                     AddDesc* __restrict__ desc, int* __restrict__ cend, unsigned long long* __restrict__ states,
+                     unsigned long long* __restrict__ ticket) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long gsz = (long long)gridDim.x * blockDim.x;
+  for (long long q = g; q < n_tiles; q += gsz) states[q] = 0ull;
+  const long long M = nnz_a + nnz_b;
+  if (g == 0) {
+    *ticket = 0ull;
+    desc[n_tiles] = AddDesc{(int)nnz_a, (int)nnz_b, 0, (int)n_cols};
+  }
+  if (g >= n_cols) return;
+  const long long a0 = __ldg(&ap[g]), a1 = __ldg(&ap[g + 1]), b0 = __ldg(&bp[g]), b1 = __ldg(&bp[g + 1]);
+  const long long ms0 = a0 + b0, ms1 = a1 + b1;
+  if (ms0 == ms1) return;
+  const long long la = a1 - a0, lb = b1 - b0;
+  for (long long t = (ms0 + kAddTile - 1) / kAddTile; t * kAddTile < ms1; t++) {
+    const long long dl = t * kAddTile - ms0;
+    // first i with A[i] > B[dl - i - 1] (A wins ties): 8-probe rounds (independent
+    // loads, the range shrinks 9x per round trip), then binary steps
+    long long lo = max(0ll, dl - lb), hi = min(dl, la);
+    while (hi - lo > 16) {
+      const long long w = hi - lo;
+      int cnt = 0;  // probes (lo + w (q+1) / 9) with A <= B: a prefix of the 8
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const long long pq = lo + w * (q + 1) / 9;
+        cnt += __ldg(&ar[a0 + pq]) <= __ldg(&br[b0 + dl - pq - 1]) ? 1 : 0;
+      }
+      const long long nlo = cnt ? lo + w * cnt / 9 + 1 : lo;
+      hi = cnt < 8 ? lo + w * (cnt + 1) / 9 : hi;
+      lo = nlo;
     }
-    int r;
-    double v;
-    if (j == lb || (i < la && __ldg(&ar[a0 + i]) < __ldg(&br[b0 + j]))) {
-      r = __ldg(&ar[a0 + i]);
-      v = __dmul_rn(alpha, __ldg(&av[a0 + i]));
-      i++;
-    } else if (i == la || __ldg(&br[b0 + j]) < __ldg(&ar[a0 + i])) {
-      r = __ldg(&br[b0 + j]);
-      v = __dmul_rn(beta, __ldg(&bv[b0 + j]));
-      j++;
-    } else {
-      r = __ldg(&ar[a0 + i]);
-      v = __dadd_rn(__dmul_rn(alpha, __ldg(&av[a0 + i])), __dmul_rn(beta, __ldg(&bv[b0 + j])));
-      i++;
-      j++;
+    while (lo < hi) {
+      const long long mid = (lo + hi) >> 1;
+      if (__ldg(&ar[a0 + mid]) <= __ldg(&br[b0 + dl - mid - 1])) lo = mid + 1;
+      else hi = mid;
     }
-    if (v != 0.0) {
-      emit(r, v);
-      produced++;
-    }
-    pos = a0 + b0 + i + j;
+    const long long i = lo, j = dl - lo;
+    AddDesc d;
+    d.ia = (int)(a0 + i);
+    d.jb = (int)(b0 + j);
+    d.skip = (i > 0 && j < lb && __ldg(&ar[a0 + i - 1]) == __ldg(&br[b0 + j])) ? 1 : 0;
+    d.col = (int)g;
+    desc[t] = d;
+  }
+  for (long long t = ms0 / kAddTile; t * kAddTile < ms1; t++) {
+    const long long e = min((t + 1) * kAddTile, M) - 1;  // the tile's last merged position
+    if (e >= ms0 && e < ms1) cend[t] = (int)g;
   }
 }
 
+// Per-thread blocks of kAddItems consecutive elements would put a warp's
+// accesses kAddItems words apart (4- to 16-way bank conflicts); every array
+// indexed by element / position is padded by one slot per 8: pad(e).
+AS_DEVICE_INLINE int pad(int e) { return e + (e >> 3); }
+constexpr int kAddPadded = kAddTile + kAddTile / 8 + 1;
+
 struct AddSmem {
-  MergeWindow W;
-  int rows[kAddChunk];
-  double vals[kAddChunk];
-  long long scan_tmp[kMThreads / 32 + 1];
-  long long cb;
+  union {
+    unsigned long long key[kAddPadded];  // A range keys [0, na), B range keys [na, n)
+    int orow[kAddPadded];                // after the merge: the tile's kept rows
+  };
+  union {
+    double val[kAddPadded];
+    double oval[kAddPadded];  // after the merge: the tile's kept values
+  };
+  union {
+    unsigned mark[kAddPadded];  // column starts (B: | 0x80000000); zero between tiles
+    unsigned excl[kAddPadded];  // after the merge: kept outputs before each merged position
+  };
+  int cms[kAddTile];  // merged start of column c_first + k, relative to the tile
+  unsigned scan_u[kAddThreads / 32 + 1];
+  int scan_i[kAddThreads / 32 + 1];
+  long long prefix;
+  long long tile;
 };
 
 struct AddArgs {
-  long long n_cols;
+  long long n_cols, M, n_tiles;
   double alpha, beta;
   const int *ap, *ar, *bp, *br;
   const double *av, *bv;
@@ -92,107 +141,315 @@ struct AddArgs {
   int* out_rows;
   double* out_vals;
   long long* info;
-  long long* cta_sums;
-  unsigned char* tcount;  // [n_chunks * kMThreads] pass-1 output count of every thread's positions
-  GridBar gb;
+  const AddDesc* desc;
+  const int* cend;
+  unsigned long long* states;
+  unsigned long long* ticket;
 };
 
-__device__ void ensure_window(AddSmem& S, const AddArgs& a, long long chunk) {
+// block-wide exclusive max-scan of unsigned values (every thread calls)
+__device__ unsigned block_exclusive_max(unsigned v, unsigned* smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  unsigned inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned n = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc = max(inc, n);
+  }
+  if (lane == 31) smem[warp] = inc;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const bool inside = S.W.n > 0 && chunk >= S.W.ms[0] && chunk < S.W.ms[S.W.n];
-    S.cb = inside ? -1 : col_of_global(a.ap, a.bp, S.W.n > 0 ? S.W.c_base : 0, a.n_cols - 1, chunk);
+  if (warp == 0) {
+    const unsigned w = lane < nwarps ? smem[lane] : 0u;
+    unsigned wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned n = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi = max(wi, n);
+    }
+    const unsigned ex = __shfl_up_sync(0xffffffffu, wi, 1);
+    if (lane < nwarps) smem[lane] = lane ? ex : 0u;
   }
   __syncthreads();
-  if (S.cb >= 0) {
-    stage_window(S.W, a.ap, a.bp, a.n_cols, S.cb);
-    __syncthreads();
+  unsigned ex_in_warp = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) ex_in_warp = 0u;
+  const unsigned res = max(smem[warp], ex_in_warp);
+  __syncthreads();
+  return res;
+}
+
+// Exclusive prefix of tile t whose aggregate is already published (the
+// look-back half of tile_lookback_warp); one full warp; publishes t's
+// inclusive prefix.
+__device__ unsigned long long add_lookback_wait(unsigned long long* states, long long t, unsigned long long aggregate) {
+  const int lane = threadIdx.x & 31;
+  if (t == 0) return 0ull;
+  unsigned long long prefix = 0;
+  long long base = t - 1;
+  while (true) {
+    const long long i = base - lane;
+    unsigned long long s = kFlagInc;  // virtual inclusive 0 before tile 0
+    if (i >= 0) {
+      do {
+        s = tile_peek(&states[i]);
+      } while ((s & 3ull) == 0ull);
+    }
+    const unsigned inc_mask = __ballot_sync(0xffffffffu, (s & 3ull) == kFlagInc);
+    const int first = inc_mask ? (__ffs(inc_mask) - 1) : 32;
+    prefix += warp_reduce_sum((lane <= first) ? (s >> 2) : 0ull);
+    if (inc_mask) break;
+    base -= 32;
+  }
+  __threadfence();
+  if (lane == 0) tile_publish(&states[t], prefix + aggregate, kFlagInc);
+  return prefix;
+}
+
+// A tile's inputs, loaded into registers ahead of its turn: descriptors,
+// kAddItems rows / values per thread (element tid + u * kAddThreads) and the
+// column pointers of column c_first + tid.
+struct AddPrefetch {
+  AddDesc d0, d1;
+  int c_last, own_lo;
+  unsigned rr[kAddItems];
+  double vv[kAddItems];
+  int as_, ae, bs, be;
+};
+
+__device__ __forceinline__ void add_prefetch(const AddArgs& a, long long t, AddPrefetch& P) {
+  const int tid = threadIdx.x;
+  P.d0 = a.desc[t];
+  P.d1 = a.desc[t + 1];
+  P.c_last = __ldg(&a.cend[t]);
+  P.own_lo = t == 0 ? 0 : __ldg(&a.cend[t - 1]) + 1;
+  const int ia0 = P.d0.ia, jb0 = P.d0.jb, na = P.d1.ia - ia0, n = na + P.d1.jb - jb0;
+#pragma unroll
+  for (int u = 0; u < kAddItems; u++) {
+    const int e = tid + u * kAddThreads;
+    const bool isa = e < na;
+    const int* rp = isa ? a.ar + ia0 + e : a.br + jb0 + (e - na);
+    const double* vp = isa ? a.av + ia0 + e : a.bv + jb0 + (e - na);
+    P.rr[u] = e < n ? (unsigned)__ldg(rp) : 0u;
+    P.vv[u] = e < n ? __ldcs(vp) : 0.0;
+  }
+  const long long c = (long long)P.d0.col + tid;
+  if (c <= P.c_last) {
+    P.as_ = __ldg(&a.ap[c]);
+    P.ae = __ldg(&a.ap[c + 1]);
+    P.bs = __ldg(&a.bp[c]);
+    P.be = __ldg(&a.bp[c + 1]);
   }
 }
 
-__global__ void __launch_bounds__(kMThreads) csc_add_kernel(AddArgs a) {
+// Persistent: each CTA takes tiles by ticket until none is left.  The next
+// tile's ticket is taken as soon as this tile's count is published, and its
+// inputs are in flight while this tile looks back and writes.
+__global__ void __launch_bounds__(kAddThreads, AS_ADD_MINB) add_tile_kernel(AddArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   AddSmem& S = *reinterpret_cast<AddSmem*>(smem_raw);
   const int tid = threadIdx.x;
-  unsigned gen = 0;
-  const long long M = mstart_of(a.ap, a.bp, a.n_cols);
-  const long long per = ((M + gridDim.x - 1) / gridDim.x + kAddChunk - 1) / kAddChunk * kAddChunk;
-  const long long lo = min(M, (long long)blockIdx.x * per), hi = min(M, lo + per);
-  if (tid == 0) {
-    S.W.n = 0;
-    S.W.c_base = 0;
-  }
-  auto no_col = [](long long, int) {};
+  for (int e = tid; e < kAddPadded; e += kAddThreads) S.mark[e] = 0u;
+  if (tid == 0) S.tile = (long long)atomicAdd(a.ticket, 1ull);
+  __syncthreads();
+  long long t = S.tile;
+  AddPrefetch P;
+  if (t < a.n_tiles) add_prefetch(a, t, P);
+  while (t < a.n_tiles) {
+    const AddDesc d0 = P.d0, d1 = P.d1;
+    const long long c_first = d0.col, c_last = P.c_last, own_lo = P.own_lo;
+    const int ia0 = d0.ia, jb0 = d0.jb;
+    const int na = d1.ia - ia0, nb = d1.jb - jb0, n = na + nb;
+    const long long tpos = t * kAddTile;
+    const long long span = c_last - c_first + 1;
 
-  // pass 1: count
-  long long total = 0;
-  for (long long chunk = lo; chunk < hi; chunk += kAddChunk) {
-    ensure_window(S, a, chunk);
-    const long long d0 = chunk + (long long)tid * kAddItems;
-    const long long d1 = min(d0 + kAddItems, min(hi, chunk + kAddChunk));
-    int cnt = 0;
-    if (d0 < d1)
-      merge_range(a.n_cols, col_of(S.W, a.ap, a.bp, a.n_cols, d0), d0, d1, a.ap, a.ar, a.av, a.bp, a.br, a.bv, a.alpha,
-                  a.beta, [&](int, double) { cnt++; }, no_col);
-    a.tcount[(chunk / kAddChunk) * kMThreads + tid] = (unsigned char)cnt;  // reused by pass 2
-    total += block_reduce_sum<long long>((long long)cnt, S.scan_tmp);
-  }
-  if (tid == 0) a.cta_sums[blockIdx.x] = total;
-  grid_sync(a.gb, gen);
-  long long pre = 0;
-  for (long long q = tid; q < blockIdx.x; q += blockDim.x) pre += a.cta_sums[q];
-  pre = block_reduce_sum<long long>(pre, S.scan_tmp);
-
-  // pass 2: write, staged through shared memory
-  long long run = pre;
-  for (long long chunk = lo; chunk < hi; chunk += kAddChunk) {
-    ensure_window(S, a, chunk);
-    const long long d0 = chunk + (long long)tid * kAddItems;
-    const long long d1 = min(d0 + kAddItems, min(hi, chunk + kAddChunk));
-    const long long c0 = d0 < d1 ? col_of(S.W, a.ap, a.bp, a.n_cols, d0) : 0;
-    const int cnt = __ldcg(&a.tcount[(chunk / kAddChunk) * kMThreads + tid]);
-    long long ctot;
-    const long long off = block_exclusive_scan<long long>((long long)cnt, S.scan_tmp, &ctot);
-    int w = (int)off;
-    if (d0 < d1)
-      merge_range(
-          a.n_cols, c0, d0, d1, a.ap, a.ar, a.av, a.bp, a.br, a.bv, a.alpha, a.beta,
-          [&](int r, double v) {
-            S.rows[w] = r;
-            S.vals[w] = v;
-            w++;
-          },
-          [&](long long c, int produced) { a.out_ptr[c] = (int)(run + off + produced); });
-    __syncthreads();
-    for (long long q = tid; q < ctot; q += blockDim.x) {
-      a.out_rows[run + q] = S.rows[q];
-      a.out_vals[run + q] = S.vals[q];
+    // 1. rows, values and the column starts of the tile's A and B ranges
+#pragma unroll
+    for (int u = 0; u < kAddItems; u++) {
+      const int e = tid + u * kAddThreads;
+      if (e < n) {
+        S.key[pad(e)] = P.rr[u];
+        S.val[pad(e)] = P.vv[u];
+      }
     }
-    run += ctot;
-  }
-  // columns starting at M (empty trailing ones) and the final offset
-  if (blockIdx.x == gridDim.x - 1) {
+    for (long long k = tid; k < span; k += kAddThreads) {
+      const long long c = c_first + k;
+      int as_, ae, bs, be;
+      if (k == tid) {
+        as_ = P.as_;
+        ae = P.ae;
+        bs = P.bs;
+        be = P.be;
+      } else {  // tiles spanning more than kAddThreads columns
+        as_ = __ldg(&a.ap[c]);
+        ae = __ldg(&a.ap[c + 1]);
+        bs = __ldg(&a.bp[c]);
+        be = __ldg(&a.bp[c + 1]);
+      }
+      if (as_ < ae && ae > ia0 && as_ < ia0 + na) S.mark[pad(max(as_, ia0) - ia0)] = (unsigned)c;
+      if (bs < be && be > jb0 && bs < jb0 + nb) S.mark[pad(na + max(bs, jb0) - jb0)] = (unsigned)c | 0x80000000u;
+      if (span <= kAddTile) S.cms[k] = (int)((long long)as_ + bs - tpos);
+    }
     __syncthreads();
-    if (tid == 0) S.cb = M > 0 ? col_of_global(a.ap, a.bp, 0, a.n_cols - 1, M - 1) + 1 : 0;
+    {  // columns: inclusive max-scan of the marks (B's marks dominate A's); marks re-zeroed
+      const int e0 = tid * kAddItems;
+      unsigned m[kAddItems];
+      unsigned run = 0u;
+#pragma unroll
+      for (int u = 0; u < kAddItems; u++) {
+        m[u] = e0 + u < n ? S.mark[pad(e0 + u)] : 0u;
+        if (e0 + u < n) S.mark[pad(e0 + u)] = 0u;
+        run = max(run, m[u]);
+      }
+      unsigned ex = block_exclusive_max(run, S.scan_u);
+#pragma unroll
+      for (int u = 0; u < kAddItems; u++) {
+        ex = max(ex, m[u]);
+        if (e0 + u < n) S.key[pad(e0 + u)] |= (unsigned long long)(ex & 0x7fffffffu) << 32;
+      }
+    }
     __syncthreads();
-    const long long total_all = pre + total;
-    for (long long c = S.cb + tid; c <= a.n_cols; c += blockDim.x) a.out_ptr[c] = (int)total_all;
-    if (tid == 0) a.info[0] = total_all;
+
+    // 2. merge kAddItems positions per thread
+    auto kA = [&](int x) { return S.key[pad(x)]; };
+    auto kB = [&](int x) { return S.key[pad(na + x)]; };
+    auto vA = [&](int x) { return S.val[pad(x)]; };
+    auto vB = [&](int x) { return S.val[pad(na + x)]; };
+    const int p0 = tid * kAddItems;
+    int i = 0, j = 0;
+    if (p0 < n) {
+      int lo = max(0, p0 - nb), hi = min(p0, na);
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (kA(mid) <= kB(p0 - mid - 1)) lo = mid + 1;
+        else hi = mid;
+      }
+      i = lo;
+      j = p0 - lo;
+    }
+    // walk with the current A / B keys in registers (~0 = exhausted) and the
+    // key of the A element consumed last (a B element equal to it was summed
+    // into it and emits nothing)
+    constexpr unsigned long long kNone = ~0ull;
+    unsigned long long ka = i < na ? kA(i) : kNone, kb = j < nb ? kB(j) : kNone;
+    unsigned long long last_a = i > 0 ? kA(i - 1) : (j == 0 && d0.skip ? kb : kNone);
+    int orow[kAddItems];
+    double oval[kAddItems];
+    unsigned keep = 0u;
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < kAddItems; u++) {
+      if (p0 + u < n) {
+        bool emit = true;
+        double v;
+        if (ka <= kb) {
+          const double av = vA(i);
+          if (ka == kb || (kb == kNone && i == na - 1 && d1.skip)) {
+            const double bv = kb != kNone ? vB(j) : __ldg(&a.bv[d1.jb]);
+            v = __dadd_rn(__dmul_rn(a.alpha, av), __dmul_rn(a.beta, bv));
+          } else {
+            v = __dmul_rn(a.alpha, av);
+          }
+          orow[u] = (int)(unsigned)ka;
+          last_a = ka;
+          i++;
+          ka = i < na ? kA(i) : kNone;
+        } else {
+          emit = kb != last_a;
+          v = __dmul_rn(a.beta, vB(j));
+          orow[u] = (int)(unsigned)kb;
+          j++;
+          kb = j < nb ? kB(j) : kNone;
+        }
+        oval[u] = v;
+        if (emit && v != 0.0) {
+          keep |= 1u << u;
+          cnt++;
+        }
+      }
+    }
+    int total;
+    const int off = block_exclusive_scan<int>(cnt, S.scan_i, &total);  // (its barriers end every merge)
+    {
+      int run = off;
+#pragma unroll
+      for (int u = 0; u < kAddItems; u++) {
+        if (p0 + u < n) S.excl[pad(p0 + u)] = (unsigned)run;
+        if (keep >> u & 1u) {
+          S.orow[pad(run)] = orow[u];
+          S.oval[pad(run)] = oval[u];
+          run++;
+        }
+      }
+      if (tid == 0) S.excl[pad(n)] = (unsigned)total;
+    }
+
+    // 3. publish the count, take the next ticket and start its loads, then
+    //    look back for the output offset and write
+    if (tid == 0) {
+      tile_publish(&a.states[t], (unsigned long long)total, t == 0 ? kFlagInc : kFlagAgg);
+      S.tile = (long long)atomicAdd(a.ticket, 1ull);
+    }
+    __syncthreads();
+    const long long tn = S.tile;
+    if (tn < a.n_tiles) add_prefetch(a, tn, P);
+    if (tid < 32) {
+      const unsigned long long pre = add_lookback_wait(a.states, t, (unsigned long long)total);
+      if (tid == 0) S.prefix = (long long)pre;
+    }
+    __syncthreads();
+    const long long base = S.prefix;
+    for (int q = tid; q < total; q += kAddThreads) {
+      __stcs(&a.out_rows[base + q], S.orow[pad(q)]);
+      __stcs(&a.out_vals[base + q], S.oval[pad(q)]);
+    }
+    // col_ptr of the columns whose merged start lies in this tile: (cend[t-1], c_last],
+    // and for the last tile every column up to n_cols
+    const bool last = t == a.n_tiles - 1;
+    const long long own_hi = last ? a.n_cols : c_last;
+    for (long long c = own_lo + tid; c <= own_hi; c += kAddThreads) {
+      int rel;
+      if (c < c_first) rel = 0;  // empty columns before the tile's first one
+      else if (c > c_last) rel = n;
+      else if (span <= kAddTile) rel = S.cms[c - c_first];
+      else rel = (int)((long long)__ldg(&a.ap[c]) + __ldg(&a.bp[c]) - tpos);
+      a.out_ptr[c] = (int)(base + S.excl[pad(rel)]);
+    }
+    if (last && tid == 0) a.info[0] = base + total;
+    __syncthreads();  // the staging is free for the next tile
+    t = tn;
   }
 }
 
-static int add_grid() {
-  static int grid[kMaxDevices] = {0};  // per device: the attribute and occupancy are per device
+struct AddWs {
+  unsigned long long* ticket;
+  unsigned long long* states;
+  AddDesc* desc;
+  int* cend;
+};
+
+static AddWs carve_add(void* ws, size_t cap, long long n_tiles, size_t* need) {
+  Carve cv(ws, cap);
+  AddWs w;
+  w.ticket = cv.take<unsigned long long>(1);
+  w.states = cv.take<unsigned long long>((size_t)n_tiles + 1);
+  w.desc = cv.take<AddDesc>((size_t)n_tiles + 1);
+  w.cend = cv.take<int>((size_t)n_tiles + 1);
+  if (need) *need = cv.off;
+  return w;
+}
+
+// resident CTAs of the persistent tile kernel (per device; 0 = cannot configure)
+static int add_resident() {
+  static int grid[kMaxDevices] = {0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
   if (grid[dev] == 0) {
     int per_sm = 0, sms = 0;
-    if (cudaFuncSetAttribute(csc_add_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(AddSmem)) !=
+    if (cudaFuncSetAttribute(add_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(AddSmem)) !=
         cudaSuccess)
       return 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csc_add_kernel, kMThreads, sizeof(AddSmem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, add_tile_kernel, kAddThreads, sizeof(AddSmem));
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid[dev] = std::max(1, std::min(per_sm * sms, 148 * 8));
+    grid[dev] = std::max(1, per_sm * sms);
   }
   return grid[dev];
 }
@@ -205,8 +462,10 @@ extern "C" {
 
 size_t as_add_workspace_bytes(int64_t n_cols, int64_t nnz_a, int64_t nnz_b) {
   (void)n_cols;
-  const long long n_chunks = (nnz_a + nnz_b + kAddChunk - 1) / kAddChunk;
-  return 256 + (size_t)148 * 8 * sizeof(long long) + (size_t)(n_chunks + 1) * kMThreads;
+  const long long n_tiles = (nnz_a + nnz_b + kAddTile - 1) / kAddTile;
+  size_t need = 0;
+  carve_add(nullptr, 0, n_tiles, &need);
+  return need;
 }
 
 int as_csc_add_f64(int64_t n_rows, int64_t n_cols, double alpha, double beta, const int32_t* a_col_ptr,
@@ -214,14 +473,28 @@ int as_csc_add_f64(int64_t n_rows, int64_t n_cols, double alpha, double beta, co
                    const double* b_vals, int64_t nnz_a, int64_t nnz_b, int32_t* col_ptr, int32_t* row_idx,
                    double* out_vals, int64_t* info, void* ws, size_t ws_bytes, void* stream) {
   cudaStream_t st = S(stream);
-  AS_REQUIRE(n_rows >= 0 && n_cols >= 0, AS_ERR_SHAPE, "negative dimension");
+  AS_REQUIRE(n_rows >= 0 && n_cols >= 0 && nnz_a >= 0 && nnz_b >= 0, AS_ERR_SHAPE, "negative dimension");
   AS_REQUIRE(nnz_a + nnz_b <= 0x7fffffffll, AS_ERR_ARG, "nnz outside the int32 range");
   AS_REQUIRE(ws_bytes >= as_add_workspace_bytes(n_cols, nnz_a, nnz_b), AS_ERR_ARG, "workspace too small");
-  const int grid = add_grid();
-  AS_REQUIRE(grid > 0, AS_ERR_CUDA, "cannot configure the add kernel");
-  AS_CUDA_TRY(cudaMemsetAsync(ws, 0, 256, st));
+  const int resident = add_resident();
+  AS_REQUIRE(resident > 0, AS_ERR_CUDA, "cannot configure the add kernel");
+  const long long M = nnz_a + nnz_b;
+  const long long n_tiles = (M + kAddTile - 1) / kAddTile;
+  if (n_tiles == 0) {
+    AS_CUDA_TRY(cudaMemsetAsync(col_ptr, 0, (size_t)(n_cols + 1) * sizeof(int32_t), st));
+    AS_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int64_t), st));
+    return AS_OK;
+  }
+  const AddWs w = carve_add(ws, ws_bytes, n_tiles, nullptr);
+  const long long part_threads = std::max((long long)n_cols, n_tiles);
+  add_partition_kernel<<<(unsigned)((part_threads + kAddPartThreads - 1) / kAddPartThreads), kAddPartThreads, 0,
+                         st>>>(n_cols, nnz_a, nnz_b, n_tiles, a_col_ptr, a_row_idx, b_col_ptr, b_row_idx, w.desc, w.cend,
+                               w.states, w.ticket);
+  AS_LAUNCH_CHECK();
   AddArgs a;
   a.n_cols = n_cols;
+  a.M = M;
+  a.n_tiles = n_tiles;
   a.alpha = alpha;
   a.beta = beta;
   a.ap = a_col_ptr;
@@ -234,12 +507,12 @@ int as_csc_add_f64(int64_t n_rows, int64_t n_cols, double alpha, double beta, co
   a.out_rows = row_idx;
   a.out_vals = out_vals;
   a.info = (long long*)info;
-  a.cta_sums = (long long*)((char*)ws + 256);
-  a.tcount = (unsigned char*)(a.cta_sums + 148 * 8);
-  a.gb = GridBar{(unsigned*)ws, (unsigned*)ws + 32};
-  void* args[] = {(void*)&a};
-  AS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)csc_add_kernel, dim3(grid), dim3(kMThreads), args,
-                                          sizeof(AddSmem), st));
+  a.desc = w.desc;
+  a.cend = w.cend;
+  a.states = w.states;
+  a.ticket = w.ticket;
+  add_tile_kernel<<<(unsigned)std::min<long long>(n_tiles, resident), kAddThreads, sizeof(AddSmem), st>>>(a);
+  AS_LAUNCH_CHECK();
   return AS_OK;
 }
 

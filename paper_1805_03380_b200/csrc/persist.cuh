@@ -1158,48 +1158,6 @@ __device__ void pre_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a,
   __syncthreads();
 }
 
-// Executed by one full warp of the tile: the exclusive prefix of bucket t's
-// kept count over buckets [0, t).  Each bucket publishes its count to st[t]
-// and adds it to its group word grp[t / 32] (publishers << 56 | sum); the
-// prefix is the completed words of the preceding groups plus the in-group
-// predecessors -- two parallel polls.  (A chained look-back walked back up to
-// n_cb / 32 serial rounds: the tiles of a wave reach this point together, so
-// few inclusive prefixes were ever published in time.)  Tickets are handed
-// out in bucket order by co-resident CTAs, so every predecessor is running.
-__device__ __forceinline__ unsigned long long group_lookback_warp(unsigned long long* st, unsigned long long* grp,
-                                                                  long long t, unsigned long long kept) {
-  const int lane = threadIdx.x & 31;
-  constexpr unsigned long long kOne = 1ull << 56, kSum = kOne - 1;
-  if (lane == 0) {
-    atomicExch(&st[t], (kept << 1) | 1ull);
-    atomicAdd(&grp[t >> 5], kOne | kept);
-  }
-  unsigned long long pre = 0;
-  const long long q = (t & ~31ll) + lane;  // in-group predecessor of this lane
-  if (q < t) {
-    unsigned long long s;
-    do {
-      s = tile_peek(&st[q]);
-    } while (!(s & 1ull));
-    pre = s >> 1;
-  }
-  const long long ng = t >> 5;  // complete groups before t's
-  for (long long i0 = 0; i0 < ng; i0 += 32 * 4) {
-    unsigned long long v[4];
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const long long i = i0 + lane + 32 * u;
-      v[u] = i < ng ? tile_peek(&grp[i]) : 32 * kOne;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const long long i = i0 + lane + 32 * u;
-      while ((v[u] >> 56) < 32) v[u] = tile_peek(&grp[i]);
-      pre += v[u] & kSum;
-    }
-  }
-  return warp_reduce_sum(pre);
-}
 
 template <class T, class S1, class S2, bool kTwo = false>
 __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_kernel(PersistArgs<T, S1, S2> a) {

@@ -123,6 +123,32 @@ def test_add_with_empty_and_cancelling(K, rng):
         assert_csc_equal(_np(got), oracle.linear_combine(30, *x, *y, al, be), exact_values=True)
 
 
+def test_add_tile_boundaries(K):
+    # the merge is cut into fixed tiles of merged positions: coincident pairs
+    # straddle tile edges, tiles span thousands of empty columns, one column
+    # spans many tiles, everything cancels
+    rng = np.random.default_rng(31)
+    a = oracle.canonicalize(2000, 2000, rng.integers(0, 2000, 300000), rng.integers(0, 2000, 300000),
+                            rng.uniform(-1, 1, 300000))
+    keep = rng.random(a[0].shape[0]) < 0.5
+    half = oracle.canonicalize(2000, 2000, a[1][keep], np.repeat(np.arange(2000), np.diff(a[2]))[keep],
+                               a[0][keep] * 3.0)
+    sparse_cols = oracle.canonicalize(50, 2000000, rng.integers(0, 50, 9000), rng.integers(0, 2000000, 9000),
+                                      rng.uniform(-1, 1, 9000))
+    sparse_cols2 = oracle.canonicalize(50, 2000000, rng.integers(0, 50, 7000), rng.integers(0, 2000000, 7000),
+                                       rng.uniform(-1, 1, 7000))
+    one_col = oracle.canonicalize(1000000, 1, rng.integers(0, 1000000, 300000), np.zeros(300000, np.int64),
+                                  rng.uniform(-1, 1, 300000))
+    one_col2 = oracle.canonicalize(1000000, 1, rng.integers(0, 1000000, 200000), np.zeros(200000, np.int64),
+                                   rng.uniform(-1, 1, 200000))
+    cases = [(2000, 2000, a, a, 1.0, 1.0), (2000, 2000, a, a, 1.0, -1.0), (2000, 2000, a, half, 1.0, 1.0),
+             (2000, 2000, half, a, -0.5, 2.0), (50, 2000000, sparse_cols, sparse_cols2, 1.0, 1.0),
+             (1000000, 1, one_col, one_col2, 1.0, 1.0), (1000000, 1, one_col, one_col, 2.0, -2.0)]
+    for n_rows, n_cols, x, y, al, be in cases:
+        got = K.linear_combine(n_rows, n_cols, _csc(x), _csc(y), al, be)
+        assert_csc_equal(_np(got), oracle.linear_combine(n_cols, *x, *y, al, be), exact_values=True)
+
+
 def test_spgemm_empty_and_zero_products(K, rng):
     a = oracle.canonicalize(20, 10, rng.integers(0, 20, 50), rng.integers(0, 10, 50), rng.uniform(-1, 1, 50))
     empty_b = oracle.canonicalize(10, 15, [], [], [])
