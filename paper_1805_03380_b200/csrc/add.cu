@@ -12,7 +12,7 @@
 // the B one emits nothing).  Merged positions are cut into tiles of kAddTile:
 //  1. add_partition_kernel, one thread per column: every tile boundary that
 //     falls inside the column gets its merge-path split (global A / B element
-//     index), the column holding it and a flag telling whether the tile's
+//     index; a warp-cooperative 32-probe search), the column holding it and a flag telling whether the tile's
 //     first B element pairs with the A element just before the tile; the
 //     column holding each tile's last position is recorded too;
 //  2. add_tile_kernel, persistent CTAs taking tiles in ticket order: the tile's A and B
@@ -57,6 +57,9 @@ add_partition_kernel(long long n_cols, long long nnz_a, long long nnz_b, long lo
                      const int* __restrict__ ar, const int* __restrict__ bp, const int* __restrict__ br,
                      AddDesc* __restrict__ desc, int* __restrict__ cend, unsigned long long* __restrict__ states,
                      unsigned long long* __restrict__ ticket) {
+  // the tile kernel may launch now (programmatic dependent launch); it waits
+  // for this grid's writes at griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;");
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long gsz = (long long)gridDim.x * blockDim.x;
   for (long long q = g; q < n_tiles; q += gsz) states[q] = 0ull;
@@ -65,44 +68,60 @@ add_partition_kernel(long long n_cols, long long nnz_a, long long nnz_b, long lo
     *ticket = 0ull;
     desc[n_tiles] = AddDesc{(int)nnz_a, (int)nnz_b, 0, (int)n_cols};
   }
-  if (g >= n_cols) return;
-  const long long a0 = __ldg(&ap[g]), a1 = __ldg(&ap[g + 1]), b0 = __ldg(&bp[g]), b1 = __ldg(&bp[g + 1]);
+  const bool valid = g < n_cols;
+  long long a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+  if (valid) {
+    a0 = __ldg(&ap[g]);
+    a1 = __ldg(&ap[g + 1]);
+    b0 = __ldg(&bp[g]);
+    b1 = __ldg(&bp[g + 1]);
+  }
   const long long ms0 = a0 + b0, ms1 = a1 + b1;
-  if (ms0 == ms1) return;
-  const long long la = a1 - a0, lb = b1 - b0;
-  for (long long t = (ms0 + kAddTile - 1) / kAddTile; t * kAddTile < ms1; t++) {
-    const long long dl = t * kAddTile - ms0;
-    // first i with A[i] > B[dl - i - 1] (A wins ties): 8-probe rounds (independent
-    // loads, the range shrinks 9x per round trip), then binary steps
+  if (valid && ms0 < ms1)
+    for (long long t = ms0 / kAddTile; t * kAddTile < ms1; t++) {
+      const long long e = min((t + 1) * kAddTile, M) - 1;  // the tile's last merged position
+      if (e >= ms0 && e < ms1) cend[t] = (int)g;
+    }
+  // Tile starts inside this thread's column, split warp-cooperatively: the
+  // warp takes the pending boundaries one at a time and locates the first
+  // i with A[i] > B[dl - i - 1] (A wins ties) with 32 probes per round trip
+  // (a 4096-entry range resolves in 3 rounds).
+  const int lane = threadIdx.x & 31;
+  long long tb = (ms0 + kAddTile - 1) / kAddTile;
+  bool pending = valid && ms0 < ms1 && tb * kAddTile < ms1;
+  while (true) {
+    const unsigned m = __ballot_sync(0xffffffffu, pending);
+    if (!m) break;
+    const int leader = __ffs(m) - 1;
+    const long long ca0 = __shfl_sync(0xffffffffu, a0, leader), cb0 = __shfl_sync(0xffffffffu, b0, leader);
+    const long long la = __shfl_sync(0xffffffffu, a1, leader) - ca0, lb = __shfl_sync(0xffffffffu, b1, leader) - cb0;
+    const long long t = __shfl_sync(0xffffffffu, tb, leader);
+    const long long dl = t * kAddTile - (ca0 + cb0);
     long long lo = max(0ll, dl - lb), hi = min(dl, la);
-    while (hi - lo > 16) {
+    while (lo < hi) {
       const long long w = hi - lo;
-      int cnt = 0;  // probes (lo + w (q+1) / 9) with A <= B: a prefix of the 8
-#pragma unroll
-      for (int q = 0; q < 8; q++) {
-        const long long pq = lo + w * (q + 1) / 9;
-        cnt += __ldg(&ar[a0 + pq]) <= __ldg(&br[b0 + dl - pq - 1]) ? 1 : 0;
+      const long long pq = w <= 32 ? lo + lane : lo + w * (lane + 1) / 33;
+      const bool le = pq < hi && __ldg(&ar[ca0 + pq]) <= __ldg(&br[cb0 + dl - pq - 1]);
+      const int cnt = __popc(__ballot_sync(0xffffffffu, le));  // a prefix of the probes
+      if (w <= 32) {
+        lo = lo + cnt;
+        break;
       }
-      const long long nlo = cnt ? lo + w * cnt / 9 + 1 : lo;
-      hi = cnt < 8 ? lo + w * (cnt + 1) / 9 : hi;
+      const long long nlo = cnt ? lo + w * cnt / 33 + 1 : lo;
+      hi = cnt < 32 ? lo + w * (cnt + 1) / 33 : hi;
       lo = nlo;
     }
-    while (lo < hi) {
-      const long long mid = (lo + hi) >> 1;
-      if (__ldg(&ar[a0 + mid]) <= __ldg(&br[b0 + dl - mid - 1])) lo = mid + 1;
-      else hi = mid;
+    if (lane == leader) {
+      const long long i = lo, j = dl - lo;
+      AddDesc d;
+      d.ia = (int)(ca0 + i);
+      d.jb = (int)(cb0 + j);
+      d.skip = (i > 0 && j < lb && __ldg(&ar[ca0 + i - 1]) == __ldg(&br[cb0 + j])) ? 1 : 0;
+      d.col = (int)g;
+      desc[t] = d;
+      tb++;
+      pending = tb * kAddTile < ms1;
     }
-    const long long i = lo, j = dl - lo;
-    AddDesc d;
-    d.ia = (int)(a0 + i);
-    d.jb = (int)(b0 + j);
-    d.skip = (i > 0 && j < lb && __ldg(&ar[a0 + i - 1]) == __ldg(&br[b0 + j])) ? 1 : 0;
-    d.col = (int)g;
-    desc[t] = d;
-  }
-  for (long long t = ms0 / kAddTile; t * kAddTile < ms1; t++) {
-    const long long e = min((t + 1) * kAddTile, M) - 1;  // the tile's last merged position
-    if (e >= ms0 && e < ms1) cend[t] = (int)g;
   }
 }
 
@@ -248,6 +267,7 @@ __global__ void __launch_bounds__(kAddThreads, AS_ADD_MINB) add_tile_kernel(AddA
   AddSmem& S = *reinterpret_cast<AddSmem*>(smem_raw);
   const int tid = threadIdx.x;
   for (int e = tid; e < kAddPadded; e += kAddThreads) S.mark[e] = 0u;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the partition kernel's writes
   if (tid == 0) S.tile = (long long)atomicAdd(a.ticket, 1ull);
   __syncthreads();
   long long t = S.tile;
@@ -511,8 +531,17 @@ int as_csc_add_f64(int64_t n_rows, int64_t n_cols, double alpha, double beta, co
   a.cend = w.cend;
   a.states = w.states;
   a.ticket = w.ticket;
-  add_tile_kernel<<<(unsigned)std::min<long long>(n_tiles, resident), kAddThreads, sizeof(AddSmem), st>>>(a);
-  AS_LAUNCH_CHECK();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)std::min<long long>(n_tiles, resident));
+  cfg.blockDim = dim3(kAddThreads);
+  cfg.dynamicSmemBytes = sizeof(AddSmem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  AS_CUDA_TRY(cudaLaunchKernelEx(&cfg, add_tile_kernel, a));
   return AS_OK;
 }
 
