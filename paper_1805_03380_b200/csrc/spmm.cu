@@ -18,8 +18,6 @@
 // Exact mode mirrors the reference's arithmetic: float64 accumulator, product
 // and sum separately rounded, columns with B[j,c] == 0 skipped, contributions
 // in ascending column order -- bit-identical to mat_times_vec for float64.
-#include <stdlib.h>
-
 #include "capi_util.cuh"
 #include "common.cuh"
 
@@ -246,68 +244,22 @@ vecmat_csc_kernel(long long n_cols, const int* __restrict__ col_ptr, const int* 
   w[j] = s;
 }
 
-// L2 residency of the dense chunk: an access-policy window over Bt marks its
-// lines persisting (A's and C's streams are evict-first), inside a persisting
-// carve-out of the L2 set once per device.  Without it the createpolicy
-// evict_last hints alone left Bt being re-read from HBM (~2.6x its size per
-// chunk).  AS_SPMM_L2WIN=0 disables it (measurement).
-static bool spmm_l2_window(const void* base, size_t bytes, cudaLaunchAttribute* attr) {
-  static int enabled = -1;
-  if (enabled < 0) {
-    const char* e = getenv("AS_SPMM_L2WIN");
-    enabled = (e && e[0] == '0') ? 0 : 1;
-  }
-  if (!enabled) return false;
-  static size_t limit[kMaxDevices] = {0};
-  static int max_win[kMaxDevices] = {0};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return false;
-  if (max_win[dev] == 0) {
-    int max_persist = 0, mw = 0;
-    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
-    cudaDeviceGetAttribute(&mw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-    size_t cur = 0;
-    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-    if (cur < (size_t)max_persist && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist) == cudaSuccess)
-      cur = (size_t)max_persist;
-    cudaGetLastError();
-    limit[dev] = cur;
-    max_win[dev] = mw > 0 ? mw : -1;
-  }
-  if (max_win[dev] < 0 || limit[dev] == 0) return false;
-  const size_t win = std::min(bytes, (size_t)max_win[dev]);
-  attr->id = cudaLaunchAttributeAccessPolicyWindow;
-  attr->val.accessPolicyWindow.base_ptr = const_cast<void*>(base);
-  attr->val.accessPolicyWindow.num_bytes = win;
-  attr->val.accessPolicyWindow.hitRatio = std::min(1.0f, (float)((double)limit[dev] / (double)win));
-  attr->val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  attr->val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  return true;
-}
-
 template <class T, int KC, bool kExact>
 static int spmm_impl(long long n_rows, long long n_cols, long long k, const int* row_ptr, const int* col_idx,
                      const T* vals, const T* B, long long ldb, T* C, long long ldc, T* Bt, cudaStream_t st) {
   constexpr int kL = KC / (16 / sizeof(T));
   const long long blocks_r = (n_rows * kL + kMmThreads - 1) / kMmThreads;
   const int blocks_c = (int)((n_cols + kMmThreads - 1) / kMmThreads);
-  cudaLaunchAttribute attr[1];
-  const bool win = spmm_l2_window(Bt, (size_t)n_cols * KC * sizeof(T), &attr[0]);
-  cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(kMmThreads);
-  cfg.stream = st;
-  cfg.attrs = attr;
-  cfg.numAttrs = win ? 1 : 0;
   for (long long k0 = 0; k0 < k; k0 += KC) {
     const int kc = (int)min((long long)KC, k - k0);
     if (n_cols > 0) {
-      cfg.gridDim = dim3(blocks_c);
-      AS_CUDA_TRY(cudaLaunchKernelEx(&cfg, dense_chunk_transpose_kernel<T, KC>, n_cols, B + k0 * ldb, ldb, kc, Bt));
+      dense_chunk_transpose_kernel<T, KC><<<blocks_c, kMmThreads, 0, st>>>(n_cols, B + k0 * ldb, ldb, kc, Bt);
+      AS_LAUNCH_CHECK();
     }
     if (n_rows > 0) {
-      cfg.gridDim = dim3((unsigned)blocks_r);
-      AS_CUDA_TRY(cudaLaunchKernelEx(&cfg, spmm_rows_lanes_kernel<T, KC, kExact>, n_rows, row_ptr, col_idx, vals,
-                                     (const T*)Bt, kc, C + k0 * ldc, ldc));
+      spmm_rows_lanes_kernel<T, KC, kExact><<<(unsigned)blocks_r, kMmThreads, 0, st>>>(n_rows, row_ptr, col_idx,
+                                                                                      vals, Bt, kc, C + k0 * ldc, ldc);
+      AS_LAUNCH_CHECK();
     }
   }
   return AS_OK;

@@ -13,13 +13,15 @@ MATCH = {
     "flush": "persist_bucket_kernel<double, CscSrc<double>, CooSrc",
     "spmm": "spmm_rows_lanes_kernel",
     "trace": "trace_partial_kernel",
-    "add": "csc_add_kernel",
+    "add": "add_tile_kernel",
     "spgemm": "persist_bucket_kernel<double, NoSrc<double>, NoSrc",
 }
 
 
 def main():
     rows = parse(sys.argv[1])
+    for r in rows:
+        r["kernel"] = r["kernel"].replace("as::", "")
     out = {}
     for op, pat in MATCH.items():
         hits = [r for r in rows if pat in r["kernel"]]
