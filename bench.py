@@ -345,12 +345,15 @@ def main_device(args):
         t = torch.tensor([sp_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         sp_total = float(t[0])
-    e2e = {"value": e2e_value, "unit": "nnz/s", "h2d_bytes_per_step": 16 * n,  # int32-narrowed indices + f64
+    packed = (n_rows - 1).bit_length() + (n_cols - 1).bit_length() <= 31  # one 32-bit key per triplet
+    e2e = {"value": e2e_value, "unit": "nnz/s", "h2d_bytes_per_step": (12 if packed else 16) * n,  # indices + f64
            "d2h_bytes_per_step": 4 * (n_cols + 1) + 12 * k,
            "ms_median": 1e3 * statistics.median(e2e_times), "ms_min": 1e3 * min(e2e_times),
            "ms_max": 1e3 * max(e2e_times),
            "path": "SpMat.from_triplets((rows i64, cols i64, vals f64) pinned host) -> CSC read back to pinned host; "
-                   "indices narrowed to int32 on host threads while the values are copied (as_upload_coo_i64)",
+                   + ("indices packed into one 32-bit key per triplet (col << 14 | row) on host threads while the "
+                      "values are copied, unpacked by a device kernel (as_upload_coo_packed)" if packed else
+                      "indices narrowed to int32 on host threads while the values are copied (as_upload_coo_i64)"),
            "host_api_path": {"value": world * n * args.steps / sp_total,
                              "ms_median": 1e3 * statistics.median(sp_times),
                              "path": "csc.canonicalize_host: the kernel reads the pinned triplets and writes the "

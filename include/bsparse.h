@@ -74,6 +74,19 @@ int as_upload_coo_i64(const int64_t *rows, const int64_t *cols, const void *vals
                       int32_t *stage_rows, int32_t *stage_cols, int32_t *d_rows, int32_t *d_cols, void *d_vals,
                       int n_threads, int n_chunks, void *stream);
 
+/* Same, for shapes whose row and column bit widths fit 31 bits together
+ * (e.g. 10k x 10k: 14 + 14): host threads pack each triplet's indices into
+ * one 32-bit key (col << row_bits | row) -- 12 instead of 16 bytes per
+ * triplet over PCIe -- and a device kernel unpacks every copied chunk into
+ * d_rows / d_cols.  Coordinates outside the shape arrive as -1 (the same
+ * first-bad-triplet report).  d_keys: device scratch of n uint32.  Returns
+ * AS_ERR_SHAPE when the bit widths do not fit (use as_upload_coo_i64).
+ */
+int as_upload_coo_packed(const int64_t *rows, const int64_t *cols, const void *vals, int64_t n,
+                         int64_t val_bytes, int64_t n_rows, int64_t n_cols, uint32_t *stage_keys,
+                         uint32_t *d_keys, int32_t *d_rows, int32_t *d_cols, void *d_vals, int n_threads,
+                         int n_chunks, void *stream);
+
 /* ---------------------------------------------------------------------------
  * Insertion-cache flush: base CSC + element-write log -> canonical CSC.
  * Replaces rbt.to_csc (rbt.py:444-458) of the tree that RbtStore.insert

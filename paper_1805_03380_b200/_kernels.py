@@ -51,13 +51,17 @@ def _upload_threads():
     return max(1, min(8, cores // 2))
 
 
-def upload_coo(rows, cols, vals, device=None):
+def upload_coo(rows, cols, vals, device=None, shape=None):
     """int64 host triplets -> device (int32 rows, int32 cols, vals) through
     as_upload_coo_i64: host threads narrow the indices into pinned staging
     while the values are copied, so 16 bytes per triplet cross PCIe instead
     of 24.  rows / cols: contiguous CPU int64 tensors (pinned or not); vals:
     CPU float tensor (pinned: copied by the same call).  An index outside
-    [0, 2^31) arrives as -1 (coo_to_csc reports it as out of range)."""
+    [0, 2^31) arrives as -1 (coo_to_csc reports it as out of range).
+    shape = (n_rows, n_cols) whose index bit widths fit 31 bits together:
+    the indices travel packed as one 32-bit key per triplet
+    (as_upload_coo_packed, 12 bytes per triplet; coordinates outside the
+    shape arrive as -1)."""
     L = _lib.lib()
     dev = _dev(device)
     n = int(rows.shape[0])
@@ -79,9 +83,18 @@ def upload_coo(rows, cols, vals, device=None):
         buf = st["buf"]
         chunks = int(os.environ.get("AS_UPLOAD_CHUNKS", "4"))
         with torch.cuda.device(dev):
-            check(L.as_upload_coo_i64(ptr(rows), ptr(cols), ptr(vals) if pinned_vals else None, n,
-                                      vals.element_size(), ptr(buf), buf.data_ptr() + 4 * n, ptr(d_rows),
-                                      ptr(d_cols), ptr(d_vals), _upload_threads(), chunks, stream()))
+            packed = shape is not None and min(shape) > 0 and \
+                (int(shape[0]) - 1).bit_length() + (int(shape[1]) - 1).bit_length() <= 31
+            if packed:
+                d_keys = torch.empty(n, dtype=torch.int32, device=dev)
+                check(L.as_upload_coo_packed(ptr(rows), ptr(cols), ptr(vals) if pinned_vals else None, n,
+                                             vals.element_size(), int(shape[0]), int(shape[1]), ptr(buf), ptr(d_keys),
+                                             ptr(d_rows), ptr(d_cols), ptr(d_vals), _upload_threads(), chunks,
+                                             stream()))
+            else:
+                check(L.as_upload_coo_i64(ptr(rows), ptr(cols), ptr(vals) if pinned_vals else None, n,
+                                          vals.element_size(), ptr(buf), buf.data_ptr() + 4 * n, ptr(d_rows),
+                                          ptr(d_cols), ptr(d_vals), _upload_threads(), chunks, stream()))
             ev = torch.cuda.Event()
             ev.record()
         st["event"] = ev

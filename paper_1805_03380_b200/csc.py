@@ -245,9 +245,10 @@ def build_device(dims: Dims, rows, cols, values, dup: str = DUP_SUM, device=None
     device = device or default_device()
     hr, hc, hv = _host_int64(rows), _host_int64(cols), _host_values(values)
     if hr is not None and hc is not None and hv is not None and torch.device(device).type == "cuda":
-        # int64 host triplets: narrowed to int32 on host threads while the
-        # values are copied (16 instead of 24 bytes per triplet over PCIe)
-        r, c, v = _kernels.upload_coo(hr, hc, hv, device)
+        # int64 host triplets: narrowed (or packed into one 32-bit key per
+        # triplet when the shape allows) on host threads while the values
+        # are copied (16 or 12 instead of 24 bytes per triplet over PCIe)
+        r, c, v = _kernels.upload_coo(hr, hc, hv, device, (dims.n_rows, dims.n_cols))
     else:
         r = _as_index_tensor(rows, device)
         c = _as_index_tensor(cols, device)

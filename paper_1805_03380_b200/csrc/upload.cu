@@ -124,7 +124,39 @@ void narrow_range(const int64_t* src, int32_t* dst, int64_t a, int64_t b) {
   for (; i < b; i++) dst[i] = narrow_index(src[i]);
 }
 
+// 32-bit keys (col << rbits | row) for coordinates inside the shape, ~0u
+// outside; streaming stores as above
+inline uint32_t pack_key(int64_t r, int64_t c, uint64_t nr, uint64_t nc, int rbits) {
+  return ((uint64_t)r < nr && (uint64_t)c < nc) ? (uint32_t)(((uint64_t)c << rbits) | (uint64_t)r) : 0xffffffffu;
+}
+
+void pack_range(const int64_t* rows, const int64_t* cols, uint32_t* dst, int64_t a, int64_t b, uint64_t nr,
+                uint64_t nc, int rbits) {
+  int64_t i = a;
+  for (; i < b && (reinterpret_cast<uintptr_t>(dst + i) & 15u); i++) dst[i] = pack_key(rows[i], cols[i], nr, nc, rbits);
+  for (; i + 4 <= b; i += 4) {
+    const __m128i q = _mm_set_epi32(
+        (int)pack_key(rows[i + 3], cols[i + 3], nr, nc, rbits), (int)pack_key(rows[i + 2], cols[i + 2], nr, nc, rbits),
+        (int)pack_key(rows[i + 1], cols[i + 1], nr, nc, rbits), (int)pack_key(rows[i], cols[i], nr, nc, rbits));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), q);
+  }
+  for (; i < b; i++) dst[i] = pack_key(rows[i], cols[i], nr, nc, rbits);
+}
+
 }  // namespace
+
+// keys[lo, hi) -> rows / cols (-1 for the out-of-shape marker)
+__global__ void __launch_bounds__(256) unpack_keys_kernel(const uint32_t* __restrict__ keys, long long lo,
+                                                          long long hi, int rbits, int32_t* __restrict__ rows,
+                                                          int32_t* __restrict__ cols) {
+  const long long i = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= hi) return;
+  const uint32_t k = __ldcs(&keys[i]);
+  const bool bad = k == 0xffffffffu;
+  rows[i] = bad ? -1 : (int32_t)(k & ((1u << rbits) - 1u));
+  cols[i] = bad ? -1 : (int32_t)(k >> rbits);
+}
+
 }  // namespace as
 
 using namespace as;
@@ -155,6 +187,35 @@ int as_upload_coo_i64(const int64_t* rows, const int64_t* cols, const void* vals
     });
     AS_CUDA_TRY(cudaMemcpyAsync(d_rows + lo, stage_rows + lo, (size_t)span * 4, cudaMemcpyHostToDevice, st));
     AS_CUDA_TRY(cudaMemcpyAsync(d_cols + lo, stage_cols + lo, (size_t)span * 4, cudaMemcpyHostToDevice, st));
+  }
+  return AS_OK;
+}
+
+int as_upload_coo_packed(const int64_t* rows, const int64_t* cols, const void* vals, int64_t n, int64_t val_bytes,
+                         int64_t n_rows, int64_t n_cols, uint32_t* stage_keys, uint32_t* d_keys, int32_t* d_rows,
+                         int32_t* d_cols, void* d_vals, int n_threads, int n_chunks, void* stream) {
+  cudaStream_t st = S(stream);
+  AS_REQUIRE(n >= 0 && (val_bytes == 4 || val_bytes == 8), AS_ERR_ARG, "bad upload arguments");
+  AS_REQUIRE(n_rows > 0 && n_cols > 0, AS_ERR_SHAPE, "packed upload needs a non-empty shape");
+  const int rbits = bits_for(n_rows - 1), cbits = bits_for(n_cols - 1);
+  AS_REQUIRE(rbits + cbits <= 31, AS_ERR_SHAPE, "%d + %d index bits do not fit a 32-bit key", rbits, cbits);
+  if (n == 0) return AS_OK;
+  const int T = std::max(1, std::min(n_threads, 256));
+  const int K = (int)std::max<int64_t>(1, std::min<int64_t>(n_chunks, (n + 65535) / 65536));
+  if (vals) AS_CUDA_TRY(cudaMemcpyAsync(d_vals, vals, (size_t)(n * val_bytes), cudaMemcpyHostToDevice, st));
+  const int64_t per = (n + K - 1) / K;
+  for (int k = 0; k < K; k++) {
+    const int64_t lo = (int64_t)k * per, hi = std::min(n, lo + per);
+    if (lo >= hi) break;
+    const int64_t span = hi - lo;
+    HostPool::get().run(T, [&](int w) {
+      const int64_t a = lo + span * w / T, b = lo + span * (w + 1) / T;
+      pack_range(rows, cols, stage_keys, a, b, (uint64_t)n_rows, (uint64_t)n_cols, rbits);
+      _mm_sfence();
+    });
+    AS_CUDA_TRY(cudaMemcpyAsync(d_keys + lo, stage_keys + lo, (size_t)span * 4, cudaMemcpyHostToDevice, st));
+    unpack_keys_kernel<<<(unsigned)((span + 255) / 256), 256, 0, st>>>(d_keys, lo, hi, rbits, d_rows, d_cols);
+    AS_LAUNCH_CHECK();
   }
   return AS_OK;
 }

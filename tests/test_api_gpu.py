@@ -360,3 +360,29 @@ def test_int64_host_upload_narrowing():
         rows[bad_pos] = bad_val
         with pytest.raises(CoordinateError, match="triplet %d " % bad_pos):
             SpMat.from_triplets(4, 4, (rows, np.zeros(6, dtype=np.int64), np.ones(6)))
+
+
+def test_packed_key_upload():
+    """Shapes whose row + column bit widths fit 31 bits move one 32-bit key per
+    triplet (as_upload_coo_packed); coordinates outside the shape (not just
+    outside int32) arrive as -1; wider shapes keep the int32 pair upload."""
+    from paper_1805_03380_b200 import _kernels
+
+    nr, nc = 1 << 16, 1 << 15  # 16 + 15 bits: the largest key is 0x7fffffff
+    rows = np.array([0, nr - 1, nr, -1, 5, nr - 1], dtype=np.int64)
+    cols = np.array([0, nc - 1, 0, 0, nc, 3], dtype=np.int64)
+    d_r, d_c, _ = _kernels.upload_coo(torch.from_numpy(rows), torch.from_numpy(cols),
+                                      torch.arange(6, dtype=torch.float64), shape=(nr, nc))
+    assert d_r.cpu().tolist() == [0, nr - 1, -1, -1, -1, nr - 1]
+    assert d_c.cpu().tolist() == [0, nc - 1, -1, -1, -1, 3]
+    rng = np.random.default_rng(78)
+    for (r, c, n) in [(nr, nc, 200000), (1 << 20, 1 << 20, 100000), (1, 1, 10), (3, 1 << 22, 1000)]:
+        rows, cols, vals = rng.integers(0, r, n), rng.integers(0, c, n), rng.uniform(-1, 1, n)
+        want = oracle.canonicalize(r, c, rows, cols, vals)
+        m = SpMat.from_triplets(r, c, (rows, cols, vals)).csc()
+        assert np.array_equal(m.col_offsets, want[2]) and np.array_equal(m.row_indices, want[1])
+        assert np.array_equal(m.values.view(np.int64), want[0].view(np.int64))
+    rows = np.zeros(9, dtype=np.int64)
+    rows[6] = 4  # == n_rows: inside int32, outside the shape
+    with pytest.raises(CoordinateError, match="triplet 6 "):
+        SpMat.from_triplets(4, 4, (rows, np.zeros(9, dtype=np.int64), np.ones(9)))
