@@ -143,21 +143,48 @@ spgemm_expand_kernel(long long nnz_b, long long n_cols_b, long long total, const
       __syncthreads();
     }
     const int cnt = (int)(P1 - P0);
-#pragma unroll 2
-    for (int q = tid; q < cnt; q += kExThreads) {
-      int ii, col;
-      double bv;
-      if (staged) {
+    auto emit = [&](long long pos, int col, unsigned row, double v) {
+      if (col >= 0) {
+        keys[pos] = ((unsigned long long)row << 32) | (unsigned long long)pos;
+        colb[pos] = (unsigned)col;
+      } else {
+        colb[pos] = row;
+      }
+      pvals[pos] = v;
+    };
+    if (staged) {
+      // kExItems products per thread: all shared-memory searches, then all
+      // gathers of A (in flight together), then the stores
+      int ii[kExItems], cl[kExItems];
+      double bv[kExItems];
+#pragma unroll
+      for (int u = 0; u < kExItems; u++) {
+        const int q = tid + u * kExThreads;
         int lo = 0, hi = nw - 1;
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
           if (s_off[mid] <= q) lo = mid;
           else hi = mid - 1;
         }
-        ii = s_ast[lo] + (q - s_off[lo]);
-        col = s_col[lo];
-        bv = s_bv[lo];
-      } else {  // many empty A columns in the window: search globally
+        ii[u] = s_ast[lo] + (q - s_off[lo]);
+        cl[u] = s_col[lo];
+        bv[u] = s_bv[lo];
+      }
+      unsigned rw[kExItems];
+      double av[kExItems];
+#pragma unroll
+      for (int u = 0; u < kExItems; u++) {
+        const bool in = tid + u * kExThreads < cnt;
+        rw[u] = in ? (unsigned)__ldg(&a_rows[ii[u]]) : 0u;
+        av[u] = in ? __ldg(&a_vals[ii[u]]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kExItems; u++) {
+        const int q = tid + u * kExThreads;
+        if (q < cnt) emit(P0 + q, cl[u], rw[u], __dmul_rn(av[u], bv[u]));
+      }
+    } else {  // many empty A columns in the window: search globally
+      for (int q = tid; q < cnt; q += kExThreads) {
         long long lo = kk0, hi = kk1;
         while (lo < hi) {
           const long long mid = (lo + hi + 1) >> 1;
@@ -165,26 +192,18 @@ spgemm_expand_kernel(long long nnz_b, long long n_cols_b, long long total, const
           else hi = mid - 1;
         }
         const int k = __ldg(&b_rows[lo]);
-        ii = (int)(__ldg(&a_ptr[k]) + (P0 + q - __ldg(&ent_ptr[lo])));
-        bv = __ldg(&b_vals[lo]);
+        const int ii = (int)(__ldg(&a_ptr[k]) + (P0 + q - __ldg(&ent_ptr[lo])));
+        const double bv = __ldg(&b_vals[lo]);
         long long cl = j0, ch = j1;
         while (cl < ch) {
           const long long mid = (cl + ch + 1) >> 1;
           if (__ldg(&b_ptr[mid]) <= lo) cl = mid;
           else ch = mid - 1;
         }
-        col = (int)cl;
+        int col = (int)cl;
+        if (dense_col(col)) col = -1 - col;
+        emit(P0 + q, col, (unsigned)__ldg(&a_rows[ii]), __dmul_rn(__ldg(&a_vals[ii]), bv));
       }
-      const long long pos = P0 + q;
-      const unsigned row = (unsigned)__ldg(&a_rows[ii]);
-      if (!staged && dense_col(col)) col = -1 - col;
-      if (col >= 0) {
-        keys[pos] = ((unsigned long long)row << 32) | (unsigned long long)pos;
-        colb[pos] = (unsigned)col;
-      } else {
-        colb[pos] = row;
-      }
-      pvals[pos] = __dmul_rn(__ldg(&a_vals[ii]), bv);
     }
   }
 }
