@@ -166,36 +166,6 @@ struct AddArgs {
   unsigned long long* ticket;
 };
 
-// block-wide exclusive max-scan of unsigned values (every thread calls)
-__device__ unsigned block_exclusive_max(unsigned v, unsigned* smem) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  unsigned inc = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned n = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc = max(inc, n);
-  }
-  if (lane == 31) smem[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    const unsigned w = lane < nwarps ? smem[lane] : 0u;
-    unsigned wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned n = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi = max(wi, n);
-    }
-    const unsigned ex = __shfl_up_sync(0xffffffffu, wi, 1);
-    if (lane < nwarps) smem[lane] = lane ? ex : 0u;
-  }
-  __syncthreads();
-  unsigned ex_in_warp = __shfl_up_sync(0xffffffffu, inc, 1);
-  if (lane == 0) ex_in_warp = 0u;
-  const unsigned res = max(smem[warp], ex_in_warp);
-  __syncthreads();
-  return res;
-}
-
 // Exclusive prefix of tile t whose aggregate is already published (the
 // look-back half of tile_lookback_warp); one full warp; publishes t's
 // inclusive prefix.

@@ -110,10 +110,11 @@ spgemm_expand_kernel(long long nnz_b, long long n_cols_b, long long total, const
   // products of a column with more than dense_min products go to the dense
   // column path of the bucket kernel, which needs only their row (in colb)
   // and value: no key, no column
-  __shared__ int s_off[kExWin];  // ent_ptr[kk] - P0 (clamped below at 0 for the first entry)
-  __shared__ int s_ast[kExWin];  // A column start of the entry, shifted to the entry's product 0
+  __shared__ unsigned s_ent[kExWin];  // range position -> its entry (marks at entry starts, then a max-scan)
+  __shared__ int s_ast[kExWin];       // A position of the entry's product q is s_ast[e] + q
   __shared__ int s_col[kExWin];
   __shared__ double s_bv[kExWin];
+  __shared__ unsigned s_scan[kExThreads / 32 + 1];
   const int tid = threadIdx.x;
   for (long long t = blockIdx.x; t * kExRange < total; t += gridDim.x) {
     const long long P0 = t * kExRange, P1 = min(total, P0 + kExRange);
@@ -123,15 +124,20 @@ spgemm_expand_kernel(long long nnz_b, long long n_cols_b, long long total, const
     const int nw = (int)(kk1 - kk0 + 1);
     const bool staged = nw <= kExWin;
     auto dense_col = [&](long long c) { return __ldg(&prod_ptr[c + 1]) - __ldg(&prod_ptr[c]) > dense_min; };
+    const int cnt = (int)(P1 - P0);
     if (staged) {
+      for (int q = tid; q < cnt; q += kExThreads) s_ent[q] = 0u;
+      __syncthreads();
       for (int e = tid; e < nw; e += kExThreads) {
         const long long kk = kk0 + e;
         const long long off = __ldg(&ent_ptr[kk]) - P0;
+        const long long end = (kk + 1 < nnz_b ? __ldg(&ent_ptr[kk + 1]) : total) - P0;
         const int k = __ldg(&b_rows[kk]);
-        // entry kk's product p sits at A position a_ptr[k] + (q - ent_ptr[kk])
-        s_off[e] = (int)max(off, 0ll);
-        s_ast[e] = (int)(__ldg(&a_ptr[k]) - min(off, 0ll));
+        // entry kk's product at range position q sits at A position a_ptr[k] + (q - off)
+        s_ast[e] = (int)(__ldg(&a_ptr[k]) - off);
         s_bv[e] = __ldg(&b_vals[kk]);
+        const long long st0 = max(off, 0ll);
+        if (min(end, (long long)cnt) > st0) s_ent[st0] = (unsigned)e;  // the one non-empty entry starting here
         long long lo = j0, hi = j1;
         while (lo < hi) {
           const long long mid = (lo + hi + 1) >> 1;
@@ -141,8 +147,23 @@ spgemm_expand_kernel(long long nnz_b, long long n_cols_b, long long total, const
         s_col[e] = dense_col(lo) ? -1 - (int)lo : (int)lo;  // negative: dense column
       }
       __syncthreads();
+      {  // every position's entry: inclusive max-scan of the marks
+        const int q0 = tid * kExItems;
+        unsigned m[kExItems], run = 0u;
+#pragma unroll
+        for (int u = 0; u < kExItems; u++) {
+          m[u] = q0 + u < cnt ? s_ent[q0 + u] : 0u;
+          run = max(run, m[u]);
+        }
+        unsigned ex = block_exclusive_max(run, s_scan);
+#pragma unroll
+        for (int u = 0; u < kExItems; u++) {
+          ex = max(ex, m[u]);
+          if (q0 + u < cnt) s_ent[q0 + u] = ex;
+        }
+      }
+      __syncthreads();
     }
-    const int cnt = (int)(P1 - P0);
     auto emit = [&](long long pos, int col, unsigned row, double v) {
       if (col >= 0) {
         keys[pos] = ((unsigned long long)row << 32) | (unsigned long long)pos;
@@ -160,15 +181,10 @@ spgemm_expand_kernel(long long nnz_b, long long n_cols_b, long long total, const
 #pragma unroll
       for (int u = 0; u < kExItems; u++) {
         const int q = tid + u * kExThreads;
-        int lo = 0, hi = nw - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (s_off[mid] <= q) lo = mid;
-          else hi = mid - 1;
-        }
-        ii[u] = s_ast[lo] + (q - s_off[lo]);
-        cl[u] = s_col[lo];
-        bv[u] = s_bv[lo];
+        const int e = q < cnt ? (int)s_ent[q] : 0;
+        ii[u] = s_ast[e] + q;
+        cl[u] = s_col[e];
+        bv[u] = s_bv[e];
       }
       unsigned rw[kExItems];
       double av[kExItems];
