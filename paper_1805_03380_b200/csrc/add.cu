@@ -188,8 +188,8 @@ __device__ unsigned long long add_lookback_wait(unsigned long long* states, long
     if (inc_mask) break;
     base -= 32;
   }
-  __threadfence();
-  if (lane == 0) tile_publish(&states[t], prefix + aggregate, kFlagInc);
+  // no fence: the state words carry only counts, nothing else is published
+  if (lane == 0) atomicExch(&states[t], ((prefix + aggregate) << 2) | kFlagInc);
   return prefix;
 }
 
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(kAddThreads, AS_ADD_MINB) add_tile_kernel(AddA
     // 3. publish the count, take the next ticket and start its loads, then
     //    look back for the output offset and write
     if (tid == 0) {
-      tile_publish(&a.states[t], (unsigned long long)total, t == 0 ? kFlagInc : kFlagAgg);
+      atomicExch(&a.states[t], ((unsigned long long)total << 2) | (t == 0 ? kFlagInc : kFlagAgg));  // (no fence needed)
       S.tile = (long long)atomicAdd(a.ticket, 1ull);
     }
     __syncthreads();

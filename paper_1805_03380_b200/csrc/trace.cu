@@ -70,7 +70,10 @@ AS_DEVICE_INLINE DD dd_shfl_xor(DD a, int o) {
 // warp lower_bound 78 us, + register lists 70 us, + filter 59 us, + deferred
 // search 53 us (instruction-issue bound: ~69% issue slots busy).
 constexpr int kTrWarpBuf = 512;
-constexpr int kTrRegs = 5;  // lists of up to 160 entries are loaded straight into registers
+#ifndef AS_TR_REGS
+#define AS_TR_REGS 5
+#endif
+constexpr int kTrRegs = AS_TR_REGS;  // lists of up to kTrRegs * 32 entries are loaded straight into registers
 constexpr int kTrBits = 8192;  // per-warp row filter (1 KB)
 
 __global__ void __launch_bounds__(kTrThreads)
