@@ -111,9 +111,12 @@ __device__ inline unsigned block_exclusive_max(unsigned v, unsigned* smem) {
 // The tile state array and the ticket counter must be zeroed before launch.
 constexpr unsigned long long kFlagAgg = 1ull, kFlagInc = 2ull;
 
+// No memory fence: every user publishes only the count carried by the state
+// word itself (outputs are written after the prefix is known), and an atomic
+// is performed at L2 where the polling loads see it.  (Fenced publishes cost
+// the sparse add 11 us of 83.)
 AS_DEVICE_INLINE void tile_publish(unsigned long long* st, unsigned long long value,
                                    unsigned long long flag) {
-  __threadfence();
   atomicExch(st, (value << 2) | flag);
 }
 
@@ -151,7 +154,6 @@ __device__ inline unsigned long long tile_lookback_warp(unsigned long long* stat
     if (inc_mask) break;
     base -= 32;
   }
-  __threadfence();
   if (lane == 0) tile_publish(&states[t], prefix + aggregate, kFlagInc);
   return prefix;
 }
