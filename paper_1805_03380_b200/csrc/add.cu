@@ -194,13 +194,14 @@ __device__ unsigned long long add_lookback_wait(unsigned long long* states, long
 }
 
 // A tile's inputs, loaded into registers ahead of its turn: descriptors,
-// kAddItems rows / values per thread (element tid + u * kAddThreads) and the
-// column pointers of column c_first + tid.
+// kAddItems rows per thread (element tid + u * kAddThreads) and the column
+// pointers of column c_first + tid.  (The values go straight to shared
+// memory with cp.async when the tile starts: they are first needed by the
+// merge, two barriers later.)
 struct AddPrefetch {
   AddDesc d0, d1;
   int c_last, own_lo;
   unsigned rr[kAddItems];
-  double vv[kAddItems];
   int as_, ae, bs, be;
 };
 
@@ -216,9 +217,7 @@ __device__ __forceinline__ void add_prefetch(const AddArgs& a, long long t, AddP
     const int e = tid + u * kAddThreads;
     const bool isa = e < na;
     const int* rp = isa ? a.ar + ia0 + e : a.br + jb0 + (e - na);
-    const double* vp = isa ? a.av + ia0 + e : a.bv + jb0 + (e - na);
     P.rr[u] = e < n ? (unsigned)__ldg(rp) : 0u;
-    P.vv[u] = e < n ? __ldcs(vp) : 0.0;
   }
   const long long c = (long long)P.d0.col + tid;
   if (c <= P.c_last) {
@@ -257,9 +256,12 @@ __global__ void __launch_bounds__(kAddThreads, AS_ADD_MINB) add_tile_kernel(AddA
       const int e = tid + u * kAddThreads;
       if (e < n) {
         S.key[pad(e)] = P.rr[u];
-        S.val[pad(e)] = P.vv[u];
+        const double* vp = e < na ? a.av + ia0 + e : a.bv + jb0 + (e - na);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(&S.val[pad(e)]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(vp) : "memory");
       }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     for (long long k = tid; k < span; k += kAddThreads) {
       const long long c = c_first + k;
       int as_, ae, bs, be;
@@ -296,6 +298,7 @@ __global__ void __launch_bounds__(kAddThreads, AS_ADD_MINB) add_tile_kernel(AddA
         if (e0 + u < n) S.key[pad(e0 + u)] |= (unsigned long long)(ex & 0x7fffffffu) << 32;
       }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's values landed
     __syncthreads();
 
     // 2. merge kAddItems positions per thread
