@@ -491,11 +491,21 @@ __device__ long long bucket_chunk_reduce(BTileSmem<T>& S, long long b, int cm, l
       const unsigned row = key_row(k), col = S.scol[p];
       if (p > 0) head = row != key_row(S.sk[p - 1]) || col != S.scol[p - 1];
       else head = (b == 0) || row != key_row(gk[b - 1]) || col != gcol[b - 1] - col_base;
-      S.u.rv[p] = vslot ? vslot[S.perm[p]] : vs((unsigned long long)key_idx(k));
+      if (vslot) {  // bucket-ordered values: an asynchronous copy, so the gathers of all
+                    // iterations are in flight together (no registers held)
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(&S.u.rv[p]);
+        if constexpr (sizeof(T) == 8)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(vslot + S.perm[p]) : "memory");
+        else
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(vslot + S.perm[p]) : "memory");
+      } else {
+        S.u.rv[p] = vs((unsigned long long)key_idx(k));
+      }
     }
     const unsigned hb = __ballot_sync(0xffffffffu, head);
     if (lane == 0 && base + warp * 32 < cm) S.hbits[(base >> 5) + warp] = hb;
   }
+  if (vslot) asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
   __syncthreads();
   tt_mark(8);
   const int pb = tid * kItems, pe = min(pb + kItems, cm);
