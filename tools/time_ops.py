@@ -35,6 +35,12 @@ def main():
             p, ri, vv, _ = _kernels.coo_to_csc(n_rows, n_cols, r, c, v)
             fn = (lambda: _kernels.coo_to_csc(n_rows, n_cols, r, c, v)) if op == "build" else (
                 lambda: _kernels.transpose(n_rows, n_cols, p, ri, vv))
+        elif op == "flush":
+            nf, _, rows, cols, vals = synth.cfg2_writes()
+            base = (torch.zeros(nf + 1, dtype=torch.int32, device=dev), torch.empty(0, dtype=torch.int32, device=dev),
+                    torch.empty(0, dtype=torch.float64, device=dev))
+            r, c, v = T(rows, torch.int32), T(cols, torch.int32), T(vals, torch.float64)
+            fn = lambda: _kernels.flush_log(nf, nf, base, r, c, v)  # noqa: E731
         elif op == "spmm":
             n, _, av, ar, ao, Bm = synth.cfg3_spmm()
             csr = _kernels.transpose(n, n, T(ao, torch.int32), T(ar, torch.int32), T(av, torch.float32))
