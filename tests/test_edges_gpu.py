@@ -143,7 +143,8 @@ def test_add_tile_boundaries(K):
                                    rng.uniform(-1, 1, 200000))
     cases = [(2000, 2000, a, a, 1.0, 1.0), (2000, 2000, a, a, 1.0, -1.0), (2000, 2000, a, half, 1.0, 1.0),
              (2000, 2000, half, a, -0.5, 2.0), (50, 2000000, sparse_cols, sparse_cols2, 1.0, 1.0),
-             (1000000, 1, one_col, one_col2, 1.0, 1.0), (1000000, 1, one_col, one_col, 2.0, -2.0)]
+             (1000000, 1, one_col, one_col2, 1.0, 1.0), (1000000, 1, one_col, one_col, 2.0, -2.0),
+             (2000, 2000, a, half, 0.0, 1.0), (2000, 2000, half, a, 1.0, 0.0), (2000, 2000, a, half, 1e-300, 1e-300)]
     for n_rows, n_cols, x, y, al, be in cases:
         got = K.linear_combine(n_rows, n_cols, _csc(x), _csc(y), al, be)
         assert_csc_equal(_np(got), oracle.linear_combine(n_cols, *x, *y, al, be), exact_values=True)
