@@ -28,20 +28,79 @@ namespace as {
 
 constexpr int kGThreads = 256;
 
-// products per column of B, one warp per column
+// products per column of B, three tiers: a lane sums a column of up to
+// kCountShort entries itself (entries and A column lengths 4 at a time), the
+// warp sums a column of up to kCountLong entries together, and a longer one
+// is listed for spgemm_count_long_kernel, where a whole CTA sums it (a warp
+// walking a 4096-entry Zipf column alone was the critical path: 64
+// dependent round trips).
+constexpr int kCountShort = 64, kCountLong = 256;
+
 __global__ void __launch_bounds__(kGThreads)
 spgemm_count_kernel(long long n_cols_b, const int* __restrict__ a_ptr, const int* __restrict__ b_ptr,
-                    const int* __restrict__ b_rows, unsigned* __restrict__ counts) {
+                    const int* __restrict__ b_rows, unsigned* __restrict__ counts, unsigned* __restrict__ longs,
+                    unsigned* __restrict__ n_longs) {
   const int lane = threadIdx.x & 31;
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long j = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < n_cols_b; j += warps) {
-    unsigned long long s = 0;
-    for (int kk = b_ptr[j] + lane; kk < b_ptr[j + 1]; kk += 32) {
-      int k = b_rows[kk];
-      s += (unsigned)(a_ptr[k + 1] - a_ptr[k]);
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long j0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; j0 < n_cols_b;
+       j0 += nw * 32) {  // warp-uniform trip count
+    const long long j = j0 + lane;
+    const bool valid = j < n_cols_b;
+    const int b0 = valid ? __ldg(&b_ptr[j]) : 0, b1 = valid ? __ldg(&b_ptr[j + 1]) : 0;
+    const int len = b1 - b0;
+    if (valid && len <= kCountShort) {
+      unsigned long long s = 0;
+      for (int kk = b0; kk < b1; kk += 4) {
+        int k[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) k[u] = kk + u < b1 ? __ldg(&b_rows[kk + u]) : -1;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          if (k[u] >= 0) s += (unsigned)(__ldg(&a_ptr[k[u] + 1]) - __ldg(&a_ptr[k[u]]));
+      }
+      counts[j] = (unsigned)s;
     }
-    s = warp_reduce_sum(s);
-    if (lane == 0) counts[j] = (unsigned)s;
+    if (valid && len > kCountLong) longs[atomicAdd(n_longs, 1u)] = (unsigned)j;
+    unsigned mm = __ballot_sync(0xffffffffu, valid && len > kCountShort && len <= kCountLong);
+    while (mm) {
+      const int src = __ffs(mm) - 1;
+      mm &= mm - 1;
+      const int c0 = __shfl_sync(0xffffffffu, b0, src), c1 = __shfl_sync(0xffffffffu, b1, src);
+      unsigned long long t = 0;
+      for (int kk = c0 + lane; kk < c1; kk += 32 * 4) {
+        int k[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) k[u] = kk + 32 * u < c1 ? __ldg(&b_rows[kk + 32 * u]) : -1;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          if (k[u] >= 0) t += (unsigned)(__ldg(&a_ptr[k[u] + 1]) - __ldg(&a_ptr[k[u]]));
+      }
+      t = warp_reduce_sum(t);
+      if (lane == src) counts[j] = (unsigned)t;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kGThreads)
+spgemm_count_long_kernel(const int* __restrict__ a_ptr, const int* __restrict__ b_ptr,
+                         const int* __restrict__ b_rows, unsigned* __restrict__ counts,
+                         const unsigned* __restrict__ longs, const unsigned* __restrict__ n_longs) {
+  __shared__ long long red[kGThreads / 32 + 1];
+  const unsigned nl = *n_longs;
+  for (unsigned i = blockIdx.x; i < nl; i += gridDim.x) {
+    const unsigned j = longs[i];
+    const int b0 = __ldg(&b_ptr[j]), b1 = __ldg(&b_ptr[j + 1]);
+    long long s = 0;
+    for (int kk = b0 + threadIdx.x; kk < b1; kk += 4 * kGThreads) {
+      int k[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) k[u] = kk + u * kGThreads < b1 ? __ldg(&b_rows[kk + u * kGThreads]) : -1;
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (k[u] >= 0) s += (long long)(__ldg(&a_ptr[k[u] + 1]) - __ldg(&a_ptr[k[u]]));
+    }
+    s = block_reduce_sum<long long>(s, red);
+    if (threadIdx.x == 0) counts[j] = (unsigned)s;
   }
 }
 
@@ -237,6 +296,7 @@ size_t as_spgemm_products_workspace_bytes(int64_t n_cols_b) {
   c.take<unsigned>(64);
   c.take<unsigned long long>(tiles);
   c.take<unsigned>(n_cols_b > 0 ? n_cols_b : 1);
+  c.take<unsigned>(n_cols_b > 0 ? n_cols_b : 1);  // long-column list
   return c.off;
 }
 
@@ -253,9 +313,14 @@ int as_spgemm_products(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, cons
   unsigned long long* states = c.take<unsigned long long>(tiles);
   unsigned* counts = c.take<unsigned>(n_cols_b > 0 ? n_cols_b : 1);
   AS_CUDA_TRY(cudaMemsetAsync(ws, 0, c.off, st));
+  unsigned* longs = c.take<unsigned>(n_cols_b > 0 ? n_cols_b : 1);  // columns above kCountLong entries
+  AS_REQUIRE(c.ok, AS_ERR_ARG, "workspace too small");
   if (n_cols_b > 0) {
-    spgemm_count_kernel<<<grid_for(n_cols_b * 32, kGThreads), kGThreads, 0, st>>>(n_cols_b, a_col_ptr, b_col_ptr,
-                                                                                   b_row_idx, counts);
+    spgemm_count_kernel<<<grid_for((n_cols_b + 31) / 32 * 32, kGThreads), kGThreads, 0, st>>>(n_cols_b, a_col_ptr, b_col_ptr,
+                                                                             b_row_idx, counts, longs, ticket + 32);
+    AS_LAUNCH_CHECK();
+    spgemm_count_long_kernel<<<kNumSMs * 4, kGThreads, 0, st>>>(a_col_ptr, b_col_ptr, b_row_idx, counts, longs,
+                                                               ticket + 32);
     AS_LAUNCH_CHECK();
   }
   count_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(counts, n_cols_b, (long long*)prod_ptr, states, ticket);
