@@ -46,8 +46,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     srcs = sources()
     objs = [os.path.join(BUILD, os.path.basename(s)[:-3] + ".o") for s in srcs]
 
+    hdrs = [d for d in _deps() if not d.endswith(".cu")]
+    hdr_t = max(os.path.getmtime(h) for h in hdrs)
+
+    def fresh(src, obj):  # incremental unless forced: the object is newer than its source and every header
+        return (not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_t)
+                and not os.environ.get("AS_NVCC_EXTRA"))
+
     def compile_one(pair):
         src, obj = pair
+        if fresh(src, obj):
+            return obj
         cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

@@ -134,16 +134,19 @@ constexpr int kAddPadded = kAddTile + kAddTile / 8 + 1;
 struct AddSmem {
   union {
     unsigned long long key[kAddPadded];  // A range keys [0, na), B range keys [na, n)
-    int orow[kAddPadded];                // after the merge: the tile's kept rows
+    struct {                             // after the merge (the keys are dead):
+      int orow[kAddPadded];              //   the tile's kept rows
+      unsigned excl[kAddPadded];         //   kept outputs before each merged position
+    };
   };
   union {
     double val[kAddPadded];
     double oval[kAddPadded];  // after the merge: the tile's kept values
   };
-  union {
-    unsigned mark[kAddPadded];  // column starts (B: | 0x80000000); zero between tiles
-    unsigned excl[kAddPadded];  // after the merge: kept outputs before each merged position
-  };
+  // column starts (B: | 0x80000000).  Zero between tiles: written only below n
+  // in step 1 and re-zeroed by the max-scan that reads them, so nothing else
+  // may share this storage (a persistent CTA's next tile would read leftovers).
+  unsigned mark[kAddPadded];
   int cms[kAddTile];  // merged start of column c_first + k, relative to the tile
   unsigned scan_u[kAddThreads / 32 + 1];
   int scan_i[kAddThreads / 32 + 1];

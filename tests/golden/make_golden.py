@@ -24,7 +24,7 @@ REF = "/root/reference/pkg/src"
 if REF not in sys.path:
     sys.path.insert(0, REF)
 
-from autosparse import Dims, SpMat, _kernels, csc, ops  # noqa: E402
+from autosparse import Dims, SpMat, _kernels, csc, expr, ops  # noqa: E402
 from autosparse.hybrid import Format  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
@@ -375,10 +375,62 @@ def gen_mm(rng):
     save("mm", cases)
 
 
+def gen_sprandu():
+    """ops.sprandu(n_rows, n_cols, density, seed) (ops.py:400-417) with its
+    sampler _sample_positions (ops.py:377-397): sparse targets (batched
+    rejection, several rounds), the dense branch (k > cells // 2 ->
+    permutation), empty and full."""
+    cases = []
+    for (r, c, dens, seed) in [(50, 40, 0.01, 1), (50, 40, 0.3, 2), (50, 40, 0.5, 3), (50, 40, 0.51, 4),
+                               (50, 40, 0.9, 5), (30, 30, 1.0, 6), (30, 30, 0.0, 7), (1000, 700, 0.002, 8),
+                               (1000, 700, 0.05, 9), (1, 500, 0.7, 10), (500, 1, 0.2, 11), (200, 300, 0.45, 12)]:
+        d = ops.sprandu(r, c, dens, seed=seed).csc()
+        cases.append(dict(r=r, c=c, density=dens, seed=seed, out_vals=d.values, out_rows=d.row_indices,
+                          out_offs=d.col_offsets))
+    save("sprandu", cases)
+
+
+EXPRS = {
+    # name -> builder over leaves a, b, c (all the same square shape)
+    "half_sum_times_ct": lambda a, b, c: expr.Mul(expr.ScalarMul(0.5, expr.Add(a, b)), expr.Transpose(c)),
+    "at_times_b": lambda a, b, c: expr.Mul(expr.Transpose(a), b),
+    "a_times_bt": lambda a, b, c: expr.Mul(a, expr.Transpose(b)),
+    "at_times_bt": lambda a, b, c: expr.Mul(expr.Transpose(a), expr.Transpose(b)),
+    "trace_at_b": lambda a, b, c: expr.Trace(expr.Mul(expr.Transpose(a), b)),
+    "trace_ab": lambda a, b, c: expr.Trace(expr.Mul(a, b)),
+    "double_t_plus": lambda a, b, c: expr.Add(expr.Transpose(expr.Transpose(a)), b),
+    "scaled_diff": lambda a, b, c: expr.ScalarMul(2.0, expr.ScalarMul(3.0, expr.Sub(a, b))),
+    "sum_times_sum_t": lambda a, b, c: expr.Mul(expr.Add(a, c), expr.Transpose(expr.Sub(b, c))),
+}
+
+
+def gen_expr(rng):
+    """expr.evaluate / evaluate_counting (expr.py:159-280) on
+    seeded operands, optimised and naive: the result (CSC or scalar) and the
+    intermediate count."""
+    cases = []
+    for (n, dens) in [(14, 0.3), (60, 0.05), (200, 0.02)]:
+        ops_in = [rand_csc(rng, n, n, max(1, int(dens * n * n))) for _ in range(3)]
+        leaves = [expr.lift(_mat(m, n, n)) for m in ops_in]
+        for name, fn in EXPRS.items():
+            for opt in (True, False):
+                out, inter = expr.evaluate_counting(fn(*leaves), optimize=opt)
+                case = dict(name=name, n=n, optimize=int(opt), intermediates=inter)
+                for k, m in zip("abc", ops_in):
+                    case.update({k + "_vals": m[0], k + "_rows": m[1], k + "_offs": m[2]})
+                if isinstance(out, SpMat):
+                    d = out.csc()
+                    case.update(kind="mat", out_vals=d.values, out_rows=d.row_indices, out_offs=d.col_offsets)
+                else:
+                    case.update(kind="scalar", out=float(out))
+                cases.append(case)
+    save("expr", cases)
+
+
 def main(only=None):
     """No arguments: every file.  `funnel` alone: only funnel.npz (its own
     seed; the first seven share one generator stream in this order)."""
-    if not only or set(only) - {"funnel", "mm"}:
+    if not only or set(only) - {"funnel", "mm", "sprandu", "expr"}:
         rng = np.random.default_rng(20260809)
         gen_canonicalize(rng)
         gen_flush(rng)
@@ -391,6 +443,10 @@ def main(only=None):
         gen_funnel(np.random.default_rng(20261019))
     if not only or "mm" in only:
         gen_mm(np.random.default_rng(20261020))
+    if not only or "sprandu" in only:
+        gen_sprandu()
+    if not only or "expr" in only:
+        gen_expr(np.random.default_rng(20261021))
 
 
 if __name__ == "__main__":

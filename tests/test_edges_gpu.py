@@ -263,3 +263,21 @@ def test_spgemm_dense_column_cancellation_and_underflow(K):
     want = oracle.spgemm(m, *a, *b, 2)
     assert_csc_equal(_np(got), want, exact_values=True)
     assert int(want[2][1]) == 0  # column 0 cancels / underflows to nothing
+
+
+@pytest.mark.parametrize("n_rows,n_cols", [(1000, 1000), (400000, 30), (100000, 20)])
+def test_add_persistent_tile_reuse(K, n_rows, n_cols):
+    # ~2M merged positions -> ~1000 tiles of 2048, more than the resident grid
+    # (4 CTAs x 148 SMs), so persistent CTAs take second tiles; the columns are
+    # low (< 2048), where leftover per-tile shared state would read as column
+    # marks (mark / excl shared storage)
+    rng = np.random.default_rng(77)
+    n = 1100000
+    a = oracle.canonicalize(n_rows, n_cols, rng.integers(0, n_rows, n), rng.integers(0, n_cols, n),
+                            rng.uniform(-1, 1, n))
+    b = oracle.canonicalize(n_rows, n_cols, rng.integers(0, n_rows, n), rng.integers(0, n_cols, n),
+                            rng.uniform(-1, 1, n))
+    assert a[0].shape[0] + b[0].shape[0] > 2048 * 4 * 148
+    for al, be in [(1.0, 1.0), (1.0, -1.0), (0.5, 2.0)]:
+        got = K.linear_combine(n_rows, n_cols, _csc(a), _csc(b), al, be)
+        assert_csc_equal(_np(got), oracle.linear_combine(n_cols, *a, *b, al, be), exact_values=True)

@@ -126,3 +126,24 @@ def test_funnel_oracle_golden():
             same(F.normalise(a, c["r"], c["c"], p_of(c["p"]), c["dim"]), c)
         elif op == "submat":
             same(F.submat(a, c["r0"], c["r1"], c["c0"], c["c1"]), c)
+
+
+def test_sample_positions_restates_the_reference_sampler():
+    """synth.sample_positions (the restatement of ops._sample_positions,
+    ops.py:377-397) + rng.random values, canonicalised by the oracle, is the
+    reference's sprandu matrix for the same seed: the generator stream is
+    consumed identically (sparse rounds, dense permutation branch, empty)."""
+    from paper_1805_03380_b200.synth import sample_positions
+
+    for case in load_golden("sprandu"):
+        r, c = int(case["r"]), int(case["c"])
+        k = int(np.floor(float(case["density"]) * r * c + 0.5))
+        rng = np.random.default_rng(int(case["seed"]))
+        pos = sample_positions(r * c, k, rng)
+        vals = rng.random(k)
+        while (vals == 0.0).any():
+            z = vals == 0.0
+            vals[z] = rng.random(int(z.sum()))
+        got = oracle.canonicalize(r, c, pos % r, pos // r, vals)
+        assert np.array_equal(got[2], case["out_offs"]) and np.array_equal(got[1], case["out_rows"])
+        assert np.array_equal(got[0].view(np.int64), case["out_vals"].view(np.int64))
