@@ -46,12 +46,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     srcs = sources()
     objs = [os.path.join(BUILD, os.path.basename(s)[:-3] + ".o") for s in srcs]
 
-    hdrs = [d for d in _deps() if not d.endswith(".cu")]
-    hdr_t = max(os.path.getmtime(h) for h in hdrs)
+    def includes(path, seen):  # the source and every local header it includes, transitively
+        if path in seen or not os.path.exists(path):
+            return seen
+        seen.add(path)
+        for line in open(path):
+            line = line.strip()
+            if line.startswith("#include \""):
+                includes(os.path.normpath(os.path.join(os.path.dirname(path), line.split('"')[1])), seen)
+        return seen
 
-    def fresh(src, obj):  # incremental unless forced: the object is newer than its source and every header
-        return (not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_t)
-                and not os.environ.get("AS_NVCC_EXTRA"))
+    def fresh(src, obj):  # incremental unless forced: the object is newer than its source and its headers
+        if force or not os.path.exists(obj) or os.environ.get("AS_NVCC_EXTRA"):
+            return False
+        return os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in includes(src, set()))
 
     def compile_one(pair):
         src, obj = pair

@@ -126,7 +126,7 @@ def coo_to_csc(n_rows, n_cols, rows, cols, vals, dup=DUP_SUM, out=None):
         out_vals = torch.empty(max(n, 1), dtype=vals.dtype, device=dev)
     info = torch.empty(2, dtype=torch.int64, device=dev)
     ws_bytes = L.as_build_workspace_bytes(n, n_cols)
-    ws = workspace(ws_bytes, dev)
+    ws = workspace(ws_bytes, dev, key="sortreduce")
     check(f(n_rows, n_cols, n, ptr(rows), ptr(cols), idx_bytes, ptr(vals), _DUP[dup], ptr(col_ptr), ptr(row_idx),
             ptr(out_vals), ptr(info), ptr(ws), ws_bytes, stream()))
     nnz, bad = _read_info(info)
@@ -149,7 +149,7 @@ def flush_log(n_rows, n_cols, base, log_rows, log_cols, log_vals):
     out_vals = torch.empty(cap, dtype=torch.float64, device=dev)
     info = torch.empty(2, dtype=torch.int64, device=dev)
     ws_bytes = L.as_flush_workspace_bytes(nb, nl, n_cols)
-    ws = workspace(ws_bytes, dev)
+    ws = workspace(ws_bytes, dev, key="sortreduce")
     check(L.as_flush_log_f64(n_rows, n_cols, nb, ptr(b_ptr), ptr(b_rows), ptr(b_vals), nl, ptr(log_rows),
                              ptr(log_cols), ptr(log_vals), ptr(col_ptr), ptr(row_idx), ptr(out_vals), ptr(info),
                              ptr(ws), ws_bytes, stream()))
@@ -166,7 +166,7 @@ def transpose(n_rows, n_cols, col_ptr, row_idx, vals):
     t_rows = torch.empty(nnz, dtype=torch.int32, device=dev)
     t_vals = torch.empty(nnz, dtype=vals.dtype, device=dev)
     ws_bytes = L.as_transpose_workspace_bytes(nnz, n_rows)
-    ws = workspace(ws_bytes, dev)
+    ws = workspace(ws_bytes, dev, key="sortreduce")
     f = L.as_csc_transpose_f64 if vals.dtype == torch.float64 else L.as_csc_transpose_f32
     check(f(n_rows, n_cols, nnz, ptr(col_ptr), ptr(row_idx), ptr(vals), ptr(t_ptr), ptr(t_rows), ptr(t_vals),
             ptr(ws), ws_bytes, stream()))

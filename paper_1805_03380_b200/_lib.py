@@ -121,5 +121,23 @@ def stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
-def workspace(nbytes: int, device) -> torch.Tensor:
-    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+_WS_CACHE = {}
+
+
+def workspace(nbytes: int, device, key=None) -> torch.Tensor:
+    """Scratch for one library call.  With `key`, a buffer kept per (device,
+    current stream, key) and grown on demand: the sort-reduce kernel
+    (construction / flush / transpose) leaves its workspace state consistent
+    and skips re-zeroing it on the next call (sortreduce.cuh); calls on one
+    stream are ordered, so reuse is safe."""
+    nbytes = max(int(nbytes), 256)
+    if key is None or nbytes > (256 << 20):  # (large scratch is not kept)
+        return torch.empty(nbytes, dtype=torch.uint8, device=device)
+    device = torch.device(device)
+    ck = (device.index if device.index is not None else torch.cuda.current_device(),
+          torch.cuda.current_stream(device).cuda_stream, key)
+    buf = _WS_CACHE.get(ck)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _WS_CACHE[ck] = buf
+    return buf

@@ -205,5 +205,9 @@ def to_csc(t: InsertionCache) -> CscData:
 
 def from_csc(m: CscData) -> InsertionCache:
     """rbt.from_csc (rbt.py:461-476): the CSC becomes the cache's base
-    snapshot -- nothing is copied or rebuilt."""
+    snapshot -- nothing is copied or rebuilt.  The snapshot stays immutable:
+    an in-place value patch of the owning SpMat (hybrid.py:170-178) writes to
+    a copy of the values instead (SpMat.set), as the reference's separate tree
+    would not see it either."""
+    m._snap = True
     return InsertionCache(m.dims, base=m)

@@ -70,7 +70,7 @@ def _to_dev(a, dtype, device):
 class CscData:
     """Canonical CSC matrix (sorted, duplicate-free, zero-free) in HBM."""
 
-    __slots__ = ("dims", "col_ptr", "row_idx", "vals", "_host")
+    __slots__ = ("dims", "col_ptr", "row_idx", "vals", "_host", "_snap")
 
     def __init__(self, dims: Dims, col_ptr, row_idx, vals, device=None):
         if dims.n_rows > DEVICE_INDEX_MAX or dims.n_cols > DEVICE_INDEX_MAX:
@@ -82,6 +82,17 @@ class CscData:
         vdt = vals.dtype if isinstance(vals, torch.Tensor) and vals.dtype in (torch.float32, torch.float64) else torch.float64
         self.vals = _to_dev(vals, vdt, device)
         self._host = None
+        self._snap = False  # an insertion cache holds this CSC as its base snapshot (rbt.from_csc)
+
+    def own_values_copy(self) -> "CscData":
+        """The same matrix with its own value array (the index arrays are
+        immutable and shared): what an in-place value patch writes to while
+        an insertion cache still holds this one as its snapshot."""
+        c = CscData.__new__(CscData)
+        c.dims, c.col_ptr, c.row_idx, c.vals = self.dims, self.col_ptr, self.row_idx, self.vals.clone()
+        c._host = None if self._host is None else (self._host[0].copy(), self._host[1], self._host[2])
+        c._snap = False
+        return c
 
     @classmethod
     def from_reference_arrays(cls, dims: Dims, values, row_indices, col_offsets, device=None) -> "CscData":

@@ -12,6 +12,7 @@
 // persist_bucket_kernel (persist.cuh); no host synchronisation.
 #include "capi_util.cuh"
 #include "persist_host.cuh"
+#include "sortreduce_api.h"
 
 
 namespace as {
@@ -45,6 +46,11 @@ static int coo_to_csc(long long n_rows, long long n_cols, long long n, const Idx
   CooSrc<IdxT, T> s1{rows, cols, vals, n, n_rows, n_cols, 0ull, info + 1};
   const int mode = dup == AS_DUP_SUM ? kSumPairwise : kLast;
   const int row_bits = bits_for(n_rows > 0 ? n_rows - 1 : 0);
+  {  // the lean single-level kernel when the input fits its envelope (device or pinned host triplets)
+    const int rc = sr::coo_to_csc<T, IdxT>(n_rows, n_cols, n, rows, cols, vals, mode, col_ptr, row_idx, out_vals, info,
+                                           ws, ws_bytes, st);
+    if (rc != -1) return rc;
+  }
   if (n > 0 && is_host_pointer(rows)) {
     // pinned host triplets: read once over PCIe inside the kernel (CooHostSrc),
     // staged in the tail of the workspace; outputs may be pinned host memory too
@@ -71,6 +77,11 @@ static int csc_transpose(long long n_rows, long long n_cols, long long nnz, cons
   AS_REQUIRE(n_rows >= 0 && n_cols >= 0 && n_rows <= kMaxDim && n_cols <= kMaxDim, AS_ERR_SHAPE,
              "dimensions %lldx%lld outside the int32 device index range", n_rows, n_cols);
   AS_REQUIRE(nnz >= 0 && nnz <= kMaxDim, AS_ERR_ARG, "nnz %lld outside the int32 range", nnz);
+  {
+    const int rc = sr::transpose<T>(n_rows, n_cols, nnz, col_ptr, row_idx, vals, t_col_ptr, t_row_idx, t_vals, ws,
+                                    ws_bytes, st);
+    if (rc != -1) return rc;
+  }
   CscSrc<T> s1{col_ptr, row_idx, vals, n_cols, nnz, true, 0ull};
   ValSrc<T> vs{vals, nullptr, (unsigned long long)nnz};
   return run_persist<T>(s1, NoSrc<T>{}, n_rows, bits_for(n_cols > 0 ? n_cols - 1 : 0), kLast, 0, vs, t_col_ptr,
@@ -85,12 +96,14 @@ extern "C" {
 
 // (includes the staging of pinned-host triplets; a device-input build uses only the first part)
 size_t as_build_workspace_bytes(int64_t n, int64_t n_cols) {
-  return persist_ws_bytes(n, n_cols, 8) + staging_bytes(n, 8);
+  return std::max(persist_ws_bytes(n, n_cols, 8) + staging_bytes(n, 8), sr::ws_bytes_api(n, 8));
 }
 size_t as_flush_workspace_bytes(int64_t nnz_base, int64_t n_log, int64_t n_cols) {
-  return persist_ws_bytes(nnz_base + n_log, n_cols, 8);
+  return std::max(persist_ws_bytes(nnz_base + n_log, n_cols, 8), sr::ws_bytes_api(nnz_base + n_log, 8));
 }
-size_t as_transpose_workspace_bytes(int64_t nnz, int64_t n_rows) { return persist_ws_bytes(nnz, n_rows, 8); }
+size_t as_transpose_workspace_bytes(int64_t nnz, int64_t n_rows) {
+  return std::max(persist_ws_bytes(nnz, n_rows, 8), sr::ws_bytes_api(nnz, 8));
+}
 
 #define AS_BUILD_DISPATCH(T)                                                                                    \
   if (idx_bytes == 4)                                                                                            \
@@ -122,6 +135,12 @@ int as_flush_log_f64(int64_t n_rows, int64_t n_cols, int64_t nnz_base, const int
              "dimensions %lldx%lld outside the int32 device index range", (long long)n_rows, (long long)n_cols);
   AS_REQUIRE(nnz_base >= 0 && n_log >= 0 && nnz_base + n_log <= kMaxDim, AS_ERR_ARG,
              "element count outside the int32 range");
+  {
+    const int rc = sr::flush_f64(n_rows, n_cols, nnz_base, base_col_ptr, base_row_idx, base_vals, n_log, log_rows,
+                                 log_cols, log_vals, col_ptr, row_idx, out_vals, (long long*)info, ws, ws_bytes,
+                                 S(stream));
+    if (rc != -1) return rc;
+  }
   CscSrc<double> s1{base_col_ptr, base_row_idx, base_vals, n_cols, nnz_base, false, 0ull};
   CooSrc<int, double> s2{log_rows, log_cols, log_vals, n_log, n_rows, n_cols, (unsigned long long)nnz_base,
                          (long long*)info + 1};

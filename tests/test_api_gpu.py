@@ -386,3 +386,17 @@ def test_packed_key_upload():
     rows[6] = 4  # == n_rows: inside int32, outside the shape
     with pytest.raises(CoordinateError, match="triplet 6 "):
         SpMat.from_triplets(4, 4, (rows, np.zeros(9, dtype=np.int64), np.ones(9)))
+
+
+def test_rbt_snapshot_not_aliased_by_in_place_patch():
+    """an RbtStore taken from a SpMat (rbt.from_csc, rbt.py:461-476)
+    is an independent store in the reference; a later in-place overwrite of
+    a stored value through the SpMat (hybrid.py:170-178) must not show in it."""
+    from paper_1805_03380_b200.cache import encode_index
+
+    m = SpMat.from_triplets(4, 3, [(0, 0, 1.0), (2, 1, 3.0), (1, 2, 2.0)])
+    t = m.rbt()
+    m.set(2, 1, 7.5)  # stored nonzero, CSC valid: patched in place
+    assert m.get(2, 1) == 7.5
+    assert t.get(encode_index(2, 1, 4)) == 3.0
+    assert m.csc().values.tolist() == [1.0, 7.5, 2.0]
