@@ -123,6 +123,54 @@ def time_oracle_build(inputs, budget_s: float):
     return reps * rows.shape[0] / el, reps, el
 
 
+REF_PKG = os.path.join(ROOT, "baseline", "_ref")
+
+
+def import_reference():
+    """The unmodified reference package (pip-installed into baseline/_ref),
+    or None when it is not there."""
+    if not os.path.isdir(os.path.join(REF_PKG, "autosparse")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/as_numba_cache")
+    if REF_PKG not in sys.path:
+        sys.path.insert(0, REF_PKG)
+    try:
+        import autosparse
+    except Exception:
+        return None
+    return autosparse
+
+
+def time_reference_build(inputs, budget_s: float):
+    """The reference's own csc.canonicalize (numpy lexsort / reduceat, one
+    thread) on the cfg 1 triplets, for ~budget_s seconds; None when the
+    reference is not installed."""
+    pkg = import_reference()
+    if pkg is None:
+        return None
+    n_rows, n_cols, rows, cols, vals = inputs
+    dims = pkg.Dims(n_rows, n_cols)
+    pkg.csc.canonicalize(dims, rows, cols, vals, "sum")  # warm (numba / numpy caches)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        pkg.csc.canonicalize(dims, rows, cols, vals, "sum")
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return {"value": reps * rows.shape[0] / el, "unit": "nnz/s", "cores": 1, "kind": "reference",
+            "sample": "%d full cfg1 builds in %.1f s: autosparse.csc.canonicalize from baseline/_ref "
+                      "(numpy/numba, single-threaded as shipped)" % (reps, el)}
+
+
+def headline_config(n_rows, n_cols, n, nnz):
+    """The `config` both arms print (identical dicts)."""
+    return {"workload": HEADLINE, "n_rows": n_rows, "n_cols": n_cols, "triplets": n, "nnz_out": nnz,
+            "values": "f64", "dup": "sum",
+            "l2": "inputs not cache-resident: device arm flushes L2 (512 MiB read) before every step; "
+                  "host arm rebuilds from DRAM-resident arrays"}
+
+
 def run_reference(args):
     """Reference arm: the reference's CPU algorithm for the headline path
     (csc.canonicalize restated in C, oracle/oracle.c) on all the host's
@@ -149,6 +197,7 @@ def run_reference(args):
     def one(_):
         oracle.canonicalize(n_rows, n_cols, rows, cols, vals, "sum")
 
+    nnz = int(oracle.canonicalize(n_rows, n_cols, rows, cols, vals, "sum")[0].shape[0])
     with ThreadPoolExecutor(max_workers=threads) as ex:
         for _ in range(args.warmup):
             list(ex.map(one, range(threads)))
@@ -163,12 +212,14 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": HEADLINE},
+        "config": headline_config(n_rows, n_cols, rows.shape[0], nnz),
         "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads, "kind": "port",
                          "sample": "per step %d concurrent full cfg1 builds, one per host thread "
                                    "(oracle/oracle.c orc_canonicalize; the reference algorithm is sequential)"
                                    % threads},
         "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        # beside the port: the reference's own numpy/numba canonicalize, one thread
+        "reference_numba": time_reference_build(inputs, min(args.cpu_budget, 5.0)),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -372,7 +423,8 @@ def main_device(args):
         rate, reps, el = time_oracle_build((n_rows, n_cols, rows, cols, vals), args.cpu_budget)
         cpu = {"value": rate, "unit": "nnz/s", "cores": 1, "kind": "port",
                "sample": "%d full cfg1 builds in %.1f s (oracle/oracle.c orc_canonicalize, 1 thread; "
-                         "os.cpu_count()=%d)" % (reps, el, os.cpu_count())}
+                         "os.cpu_count()=%d)" % (reps, el, os.cpu_count()),
+               "reference_numba": time_reference_build((n_rows, n_cols, rows, cols, vals), min(args.cpu_budget, 5.0))}
 
     if rank == 0:
         line = {
@@ -380,13 +432,12 @@ def main_device(args):
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded uniform triplets (SURVEY App. A); each rank its own batch (seed 1+rank)",
-            "config": {"workload": HEADLINE, "n_rows": n_rows, "n_cols": n_cols, "triplets": n, "nnz_out": nnz,
-                       "index_dtype": "int32 device", "l2": "flushed before every step (512 MiB device read, %s)" % args.flush,
-                       "parallelism": "independent batch per GPU" if world > 1 else "single GPU"},
+            "config": headline_config(n_rows, n_cols, n, nnz),
+            "parallelism": "independent batch per GPU" if world > 1 else "single GPU", "index_dtype": "int32 device",
             "roofline": {"bound": "hbm", "achieved": build_gbs, "peak": peak, "unit": "GB/s",
                          "frac": build_gbs / peak, "traffic": ncu_traffic("build"), "peak_source": peak_src,
-                         "traffic_source": TRAFFIC_SRC,
-                         "kernel": "as_coo_to_csc_f64 (one persistent cooperative kernel + 2 memsets)",
+                         "traffic_source": TRAFFIC_SRC, "traffic_launches": ncu_launches("build"),
+                         "kernel": "as_coo_to_csc_f64 (one cooperative sort-reduce kernel)",
                          "algorithmic_bytes": build_bytes},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 1 * args.steps, "clocks": clocks, "ops": ops,
             "ops_multi_gpu": ops_mg,
@@ -399,9 +450,10 @@ def main_device(args):
 
 
 def _load_traffic():
-    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of
-    each op's dominant kernel from the newest committed `ncu --set full`
-    capture (profiles/rNN_traffic.json, made by tools/ncu_traffic.py)."""
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of one call
+    of each op, summed over every launch of that call, from the newest
+    committed per-op `ncu --set full` captures (profiles/rNN_traffic.json,
+    made by tools/ncu_ops.sh + tools/make_traffic.py)."""
     import glob
     files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*_traffic.json")))
     if not files:
@@ -415,8 +467,14 @@ _TRAFFIC, TRAFFIC_SRC = _load_traffic()
 
 
 def ncu_traffic(op):
+    """DRAM bytes of one call of the op, summed over all its launches."""
     k = _TRAFFIC.get(op)
     return None if k is None else k["dram_read"] + k["dram_write"]
+
+
+def ncu_launches(op):
+    k = _TRAFFIC.get(op)
+    return None if k is None else k.get("launches", 1)
 
 
 def bench_mg_ops(args, dev, world, rank, l2_flush, peak):
@@ -545,7 +603,8 @@ def bench_ops(args, dev, L, sp, timed, peak):
         gbs = alg_bytes / (ms * 1e-3) / 1e9
         d = {"ms": ms, "value": units / (ms * 1e-3), "unit": unit,
              "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-                          "algorithmic_bytes": alg_bytes, "traffic": ncu_traffic(name.split("_")[0])},
+                          "algorithmic_bytes": alg_bytes, "traffic": ncu_traffic(name.split("_")[0]),
+                          "traffic_launches": ncu_launches(name.split("_")[0])},
              "parity": parity}
         if extra:
             d.update(extra)
@@ -601,6 +660,50 @@ def bench_ops(args, dev, L, sp, timed, peak):
             raise CorrectnessError("flush differs from the oracle")
         record("flush_cfg2", timed(f, K, W), nl, "writes/s", 12 * nl + 12 * nnz + 4 * (n_c + 1), "bit-exact",
                {"nnz_out": nnz, "launches": 1})
+
+    # cfg2 through the public API, as the north star states the workload:
+    # 200,000 `m[r, c] = v` element writes on a fresh SpMat, then .csc()
+    # (hybrid.py:165-181 -> rbt.py:371-387 -> rbt.to_csc rbt.py:444-458),
+    # CSC read back to the host; the reference's own SpMat beside it
+    if "flush_api" in want_ops:
+        from paper_1805_03380_b200 import SpMat
+
+        n_r, n_c, rows, cols, vals = synth.cfg2_writes()
+        rl, cl, vl = rows.tolist(), cols.tolist(), vals.tolist()
+        want = oracle.flush(n_r, n_c, (np.empty(0), np.empty(0, np.int64), np.zeros(n_c + 1, np.int64)), rows, cols,
+                            vals)
+
+        def api_run(pkg_spmat, dev_kw):
+            t0 = time.perf_counter()
+            m = pkg_spmat.zeros(n_r, n_c, **dev_kw)
+            for r_, c_, v_ in zip(rl, cl, vl):
+                m[r_, c_] = v_
+            t1 = time.perf_counter()
+            d = m.csc()
+            host = (np.asarray(d.values), np.asarray(d.row_indices), np.asarray(d.col_offsets))
+            t2 = time.perf_counter()
+            return host, t1 - t0, t2 - t1
+
+        api_run(SpMat, {"device": dev})  # warm
+        runs = [api_run(SpMat, {"device": dev}) for _ in range(3)]
+        host = runs[-1][0]
+        if not (np.array_equal(host[2], want[2]) and np.array_equal(host[1], want[1])
+                and np.array_equal(host[0], want[0])):
+            raise CorrectnessError("cfg2 API flush differs from the oracle")
+        w_ms = 1e3 * statistics.median(r[1] for r in runs)
+        f_ms = 1e3 * statistics.median(r[2] for r in runs)
+        d = {"ms": w_ms + f_ms, "writes_ms": w_ms, "csc_ms": f_ms, "value": rows.shape[0] / ((w_ms + f_ms) * 1e-3),
+             "unit": "writes/s", "parity": "bit-exact vs oracle (LastWins, 0.0 erases)",
+             "path": "SpMat.zeros; 200,000 python `m[r, c] = v` (host write log, O(1) each); .csc() = H2D of the "
+                     "log + one GPU flush + D2H of the CSC (reference-typed int64 views); wall clock"}
+        ref = import_reference() if not args.skip_slow_checks else None
+        if ref is not None:
+            h, rw, rf = api_run(ref.SpMat, {})
+            d["reference_ms"] = 1e3 * (rw + rf)
+            d["reference_writes_ms"], d["reference_csc_ms"] = 1e3 * rw, 1e3 * rf
+            d["reference_same"] = bool(np.array_equal(h[2], host[2]) and np.array_equal(h[1], host[1])
+                                       and np.array_equal(h[0], host[0]))
+        out["flush_cfg2_api"] = d
 
     # SpMM (cfg3)
     if "spmm" in want_ops:
@@ -824,7 +927,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--ops", default="transpose,flush,spmm,trace,add,spgemm,next")
+    ap.add_argument("--ops", default="transpose,flush,flush_api,spmm,trace,add,spgemm,next")
     ap.add_argument("--op-steps", type=int, default=10)
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

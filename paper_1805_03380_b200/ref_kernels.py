@@ -114,3 +114,127 @@ def rbt_to_csc(n_rows, n_cols, base, log_rows, log_cols, log_vals):
     if bad is not None:
         raise IndexError("write %d outside %dx%d matrix" % (bad, n_rows, n_cols))
     return _out(p, r, v)
+
+
+# ---------------------------------------------------------------------------
+# The two construction entry points with the reference's own types.
+#
+# csc.canonicalize(dims, rows, cols, values, dup) -> CscData (csc.py:148-193)
+# and rbt.to_csc(RbtStore) -> CscData (rbt.py:444-458) take and return the
+# reference's Dims / CscData / RbtStore objects.  The functions below keep
+# those signatures: the caller's Dims decides which CscData class comes back
+# (the class living next to it, i.e. autosparse.csc.CscData for a reference
+# caller), and the element-write store is this package's host write log
+# behind RbtStore's interface (insert / append_max / get / erase / items /
+# count / max_index), flushed to CSC by one GPU pass.
+
+
+def _csc_class_of(dims):
+    import sys
+
+    mod = sys.modules.get(type(dims).__module__)
+    cls = getattr(mod, "CscData", None)
+    if cls is None:
+        raise TypeError("no CscData next to %r" % type(dims))
+    return cls
+
+
+def _our_dims(dims):
+    from .csc import Dims
+
+    n_rows, n_cols = dims
+    return Dims(int(n_rows), int(n_cols))
+
+
+def csc_canonicalize(dims, rows, cols, values, dup="sum"):
+    """csc.canonicalize (csc.py:148-193) with its own signature: reference
+    Dims in, reference CscData out.  Coordinates are validated by the caller
+    (as in the reference); an unknown dup policy raises ValueError
+    (csc.py:184)."""
+    if dup not in ("sum", "last"):
+        raise ValueError("unknown duplicate policy %r" % (dup,))
+    n_rows, n_cols = dims
+    v, r, o = canonicalize(int(n_rows), int(n_cols), rows, cols, values, dup) if np.asarray(rows).shape[0] else (
+        np.empty(0, np.float64), np.empty(0, np.int64), np.zeros(int(n_cols) + 1, np.int64))
+    return _csc_class_of(dims)(dims, v, r, o)
+
+
+class LogStore:
+    """RbtStore (rbt.py:303-441) for a reference caller: the same methods
+    and properties over this package's write log (cache.InsertionCache);
+    `to_csc` below flushes it on the GPU.  Keeps the caller's Dims."""
+
+    def __init__(self, dims, reserve: int = 0, _base=None):
+        from .cache import InsertionCache
+
+        self.dims = dims
+        self._c = InsertionCache(_our_dims(dims), base=_base, reserve=reserve)
+
+    capacity = property(lambda self: max(16, self._c.n_writes))
+    count = property(lambda self: self._c.count)
+    max_index = property(lambda self: self._c.max_index)
+
+    def __len__(self):
+        return self._c.count
+
+    def insert(self, index, value):
+        self._c.insert(int(index), float(value))
+
+    def append_max(self, index, value):
+        self._c.append_max(int(index), float(value))
+
+    def get(self, index):
+        return self._c.get(int(index))
+
+    def erase(self, index):
+        return self._c.erase(int(index))
+
+    def items(self):
+        return self._c.items()
+
+
+def rbt_store_to_csc(t):
+    """rbt.to_csc (rbt.py:444-458): RbtStore-compatible store in, reference
+    CscData out (one GPU flush of base + write log)."""
+    m = t._c.to_csc()
+    return _csc_class_of(t.dims)(t.dims, m.values, m.row_indices, m.col_offsets)
+
+
+def rbt_from_csc(m):
+    """rbt.from_csc (rbt.py:461-476): reference CscData in; the CSC becomes
+    the store's base snapshot on the device (copied, so later in-place value
+    patches of the caller's CscData are not seen, as with the reference's
+    separate tree)."""
+    from .csc import CscData as Ours
+
+    base = Ours.from_reference_arrays(_our_dims(m.dims), np.array(m.values, np.float64),
+                                      np.array(m.row_indices, np.int64), np.array(m.col_offsets, np.int64),
+                                      device=_dev())
+    return LogStore(m.dims, _base=base)
+
+
+def install(pkg):
+    """Route a reference package (`import autosparse as pkg`) through this
+    back end: the flat-array kernel module of ops and expr, csc.canonicalize
+    (construction, also reached by csc.from_triplets / coo.to_csc /
+    SpMat.from_dense), and the element-write store with rbt.to_csc /
+    rbt.from_csc.  Returns a function that undoes the swap."""
+    import importlib
+
+    mods = {n: importlib.import_module(pkg.__name__ + "." + n) for n in ("ops", "expr", "csc", "rbt", "hybrid")}
+    import sys
+
+    me = sys.modules[__name__]
+    swaps = [(mods["ops"], "_kernels", me), (mods["expr"], "_kernels", me),
+             (mods["csc"], "canonicalize", csc_canonicalize),
+             (mods["rbt"], "RbtStore", LogStore), (mods["hybrid"], "RbtStore", LogStore),
+             (mods["rbt"], "to_csc", rbt_store_to_csc), (mods["rbt"], "from_csc", rbt_from_csc)]
+    saved = [(m, name, getattr(m, name)) for m, name, _ in swaps]
+    for m, name, new in swaps:
+        setattr(m, name, new)
+
+    def undo():
+        for m, name, old in saved:
+            setattr(m, name, old)
+
+    return undo

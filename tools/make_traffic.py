@@ -1,36 +1,38 @@
-"""profiles/r01_traffic.json from one `ncu --set full --csv --page raw`
-capture of `tools/op_runner.py all 1`: per op, the DRAM bytes and duration
-of its dominant kernel (the last matching launch)."""
+"""profiles/rNN_traffic.json from the per-op `ncu --set full` captures of
+tools/ncu_ops.sh (one NVTX-ranged call of each op per capture): per op, the
+DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) and the duration
+summed over EVERY launch of that call, plus the per-kernel breakdown.
+
+    python tools/make_traffic.py TAG out.json   (reads gpurun_out/TAG_ncu_<op>.csv)
+"""
+import glob
 import json
+import os
 import sys
 
-sys.path.insert(0, __file__.rsplit("/", 1)[0])
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from ncu_traffic import parse  # noqa: E402
-
-MATCH = {
-    "build": "persist_bucket_kernel<double, CooSrc<int",
-    "transpose": "persist_bucket_kernel<double, CscSrc<double>, NoSrc",
-    "flush": "persist_bucket_kernel<double, CscSrc<double>, CooSrc",
-    "spmm": "spmm_rows_lanes_kernel",
-    "trace": "trace_partial_kernel",
-    "add": "add_tile_kernel",
-    "spgemm": "persist_bucket_kernel<double, NoSrc<double>, NoSrc",
-}
 
 
 def main():
-    rows = parse(sys.argv[1])
-    for r in rows:
-        r["kernel"] = r["kernel"].replace("as::", "")
+    tag, dst = sys.argv[1], sys.argv[2]
     out = {}
-    for op, pat in MATCH.items():
-        hits = [r for r in rows if pat in r["kernel"]]
-        if hits:
-            out[op] = hits[-1]
-    json.dump(out, open(sys.argv[2], "w"), indent=1, sort_keys=True)
+    for path in sorted(glob.glob("gpurun_out/%s_ncu_*.csv" % tag)):
+        op = os.path.basename(path)[len(tag) + 5:-4]
+        try:
+            rows = parse(path)
+        except ValueError:
+            continue
+        if not rows:
+            continue
+        ks = [{"kernel": r["kernel"].replace("as::", "")[:90], "dram_read": r["dram_read"],
+               "dram_write": r["dram_write"], "us": r["us"]} for r in rows]
+        out[op] = {"launches": len(ks), "dram_read": sum(k["dram_read"] for k in ks),
+                   "dram_write": sum(k["dram_write"] for k in ks), "us": sum(k["us"] for k in ks), "kernels": ks}
+    json.dump(out, open(dst, "w"), indent=1, sort_keys=True)
     for op, r in sorted(out.items()):
-        print("%-10s %-60s %8.2f MB %9.2f us" % (op, r["kernel"][:60], (r["dram_read"] + r["dram_write"]) / 1e6,
-                                                 r["us"]))
+        print("%-12s %2d launches %10.2f MB %9.2f us" % (op, r["launches"], (r["dram_read"] + r["dram_write"]) / 1e6,
+                                                        r["us"]))
 
 
 if __name__ == "__main__":

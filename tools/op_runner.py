@@ -22,6 +22,13 @@ def main():
         run(o, reps)
 
 
+def rng_(op):
+    """NVTX range around one call of the op: `ncu --nvtx --nvtx-include
+    op_<name>/` then captures exactly the launches of that call
+    (tools/ncu_ops.sh), so per-op DRAM traffic is summed over all of them."""
+    return torch.cuda.nvtx.range("op_" + op)
+
+
 def run(op, reps):
     dev = torch.device("cuda")
 
@@ -33,22 +40,30 @@ def run(op, reps):
         r, c, v = T(rows, torch.int32), T(cols, torch.int32), T(vals, torch.float64)
         p, ri, vv, _ = _kernels.coo_to_csc(n_rows, n_cols, r, c, v)
         for _ in range(reps):
-            if op == "build":
-                _kernels.coo_to_csc(n_rows, n_cols, r, c, v)
-            else:
-                _kernels.transpose(n_rows, n_cols, p, ri, vv)
+            with rng_(op):
+                if op == "build":
+                    _kernels.coo_to_csc(n_rows, n_cols, r, c, v)
+                else:
+                    _kernels.transpose(n_rows, n_cols, p, ri, vv)
     elif op == "flush":
         n, _, rows, cols, vals = synth.cfg2_writes()
         base = (torch.zeros(n + 1, dtype=torch.int32, device=dev), torch.empty(0, dtype=torch.int32, device=dev),
                 torch.empty(0, dtype=torch.float64, device=dev))
+        lr, lc, lv = T(rows, torch.int32), T(cols, torch.int32), T(vals, torch.float64)
         for _ in range(reps):
-            _kernels.flush_log(n, n, base, T(rows, torch.int32), T(cols, torch.int32), T(vals, torch.float64))
-    elif op == "spmm":
+            with rng_(op):
+                _kernels.flush_log(n, n, base, lr, lc, lv)
+    elif op in ("spmm", "spmm_first"):
         n, _, av, ar, ao, B = synth.cfg3_spmm()
-        csr = _kernels.transpose(n, n, T(ao, torch.int32), T(ar, torch.int32), T(av, torch.float32))
+        a = (T(ao, torch.int32), T(ar, torch.int32), T(av, torch.float32))
+        csr = _kernels.transpose(n, n, *a)
         Bd = torch.as_tensor(B.T.copy(), device=dev).t()
         for _ in range(reps):
-            _kernels.spmm(n, n, csr, Bd)
+            with rng_(op):
+                if op == "spmm":
+                    _kernels.spmm(n, n, csr, Bd)
+                else:  # first product on a fresh CSC handle: whatever conversion it needs is part of the op
+                    _kernels.spmm_csc(n, n, a, Bd)
     elif op in ("trace", "add", "spgemm"):
         if op == "trace":
             n, _, A, B = synth.cfg4_trace_pair()
@@ -57,12 +72,13 @@ def run(op, reps):
         a = (T(A[2], torch.int32), T(A[1], torch.int32), T(A[0], torch.float64))
         b = (T(B[2], torch.int32), T(B[1], torch.int32), T(B[0], torch.float64))
         for _ in range(reps):
-            if op == "trace":
-                _kernels.fused_trace(n, n, a, b)
-            elif op == "add":
-                _kernels.linear_combine(n, n, a, b, 1.0, 1.0)
-            else:
-                _kernels.spgemm(n, n, n, a, b)
+            with rng_(op):
+                if op == "trace":
+                    _kernels.fused_trace(n, n, a, b)
+                elif op == "add":
+                    _kernels.linear_combine(n, n, a, b, 1.0, 1.0)
+                else:
+                    _kernels.spgemm(n, n, n, a, b)
     torch.cuda.synchronize()
     print("ok", op)
 
