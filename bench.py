@@ -491,7 +491,8 @@ def bench_mg_ops(args, dev, world, rank, l2_flush, peak):
     from paper_1805_03380_b200 import dist as D
 
     K, W = max(3, args.op_steps // 2), args.warmup
-    out = {"ranks": world, "collective": "NCCL all_gather (torch.distributed)"}
+    out = {"ranks": world, "collective": "NCCL via torch.distributed: all_gather (trace partials, slice sizes), "
+                                          "all_gather_into_tensor (SpMM C), grouped send/recv (gathers to rank 0)"}
 
     def T(a, dt):
         return torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
@@ -549,11 +550,13 @@ def bench_mg_ops(args, dev, world, rank, l2_flush, peak):
         k0, k1, bounds = D.spmm_block(k)
         Xb = Bd[:, k0:k1]
         lk, ck, tk = timed_pair(lambda: _kernels.spmm(n, n, csr, Xb), lambda blk: D.spmm_exchange(blk, bounds, n))
+        _, cg, tg = timed_pair(lambda: _kernels.spmm(n, n, csr, Xb), lambda blk: D.spmm_exchange(blk, bounds, n, dst=0))
         alg = 4 * (n + 1) + 8 * av.shape[0] + 8 * n * k
         return {"ms_local": lk, "ms_collective": ck, "ms": tk, "unit": "GB/s",
                 "value_compute": alg / (lk * 1e-3) / 1e9, "value": alg / (tk * 1e-3) / 1e9,
-                "note": "A replicated, dense columns split %s; C blocks all-gathered to every rank"
-                        % [int(x) for x in bounds]}
+                "ms_collective_gather0": cg, "ms_gather0": tg,
+                "note": "A replicated, dense columns split %s; C blocks all-gathered into C's column-major storage "
+                        "(all_gather_into_tensor), or sent to rank 0 (ms_gather0)" % [int(x) for x in bounds]}
 
     def spgemm_op():
         n, _, A, B = synth.cfg5_pair()
@@ -561,10 +564,15 @@ def bench_mg_ops(args, dev, world, rank, l2_flush, peak):
         b = (T(B[2], torch.int32), T(B[1], torch.int32), T(B[0], torch.float64))
         c0, c1, bounds, sb = D.spgemm_shard(a, b)
         total = int(D.spgemm_column_weights(A[2], B[2], B[1]).sum())
-        lk, ck, tk = timed_pair(lambda: _kernels.spgemm(n, n, c1 - c0, a, sb),
-                                lambda res: D.spgemm_exchange(*res, bounds))
+        local = lambda: _kernels.spgemm(n, n, c1 - c0, a, sb)
+        # left distributed (DistCsc: one all_gather of slice nnz, device-side offsets)
+        lk, ck, tk = timed_pair(local, lambda res: D.spgemm_exchange(*res, bounds, dst=None, c_range=(c0, c1)))
+        # assembled on rank 0 by grouped send/recv of the native int32 / f64 slices
+        _, cg, tg = timed_pair(local, lambda res: D.spgemm_exchange(*res, bounds, dst=0))
         return {"ms_local": lk, "ms_collective": ck, "ms": tk, "value": total / (tk * 1e-3), "unit": "products/s",
-                "value_compute": total / (lk * 1e-3), "note": "B split into %d equal-product column ranges" % world}
+                "value_compute": total / (lk * 1e-3), "ms_collective_gather0": cg, "ms_gather0": tg,
+                "note": "B split into %d equal-product column ranges; result left distributed (value) or gathered "
+                        "on rank 0 by grouped send/recv (ms_gather0)" % world}
 
     want = set(args.ops.split(","))
     if "trace" in want:

@@ -41,6 +41,11 @@ enum as_dup { AS_DUP_SUM = 0, AS_DUP_LAST = 1 }; /* csc.DUP_SUM / DUP_LAST (csc.
 
 const char *as_last_error(void);
 int as_abi_version(void);
+/* Construction / transpose engine selection (tests and measurements only):
+ * 0 = automatic (single-launch kernel up to its envelope, then the
+ * large-input pipeline, then the general bucket kernel), 1 = the large-input
+ * pipeline whenever it applies, 2 = the general bucket kernel.  Process-wide. */
+int as_set_engine(int engine);
 
 /* ---------------------------------------------------------------------------
  * COO triplets -> canonical CSC.

@@ -28,6 +28,7 @@ DBL = ctypes.c_double
 SIGNATURES = {
     "as_last_error": (ctypes.c_char_p, []),
     "as_abi_version": (INT, []),
+    "as_set_engine": (INT, [INT]),
     "as_build_workspace_bytes": (SZ, [I64, I64]),
     "as_coo_to_csc_f64": (INT, [I64, I64, I64, P, P, INT, P, INT, P, P, P, P, P, SZ, P]),
     "as_coo_to_csc_f32": (INT, [I64, I64, I64, P, P, INT, P, INT, P, P, P, P, P, SZ, P]),

@@ -13,6 +13,7 @@
 #include "capi_util.cuh"
 #include "persist_host.cuh"
 #include "sortreduce_api.h"
+#include "largen_api.h"
 
 
 namespace as {
@@ -46,7 +47,7 @@ static int coo_to_csc(long long n_rows, long long n_cols, long long n, const Idx
   CooSrc<IdxT, T> s1{rows, cols, vals, n, n_rows, n_cols, 0ull, info + 1};
   const int mode = dup == AS_DUP_SUM ? kSumPairwise : kLast;
   const int row_bits = bits_for(n_rows > 0 ? n_rows - 1 : 0);
-  {  // the lean single-level kernel when the input fits its envelope (device or pinned host triplets)
+  if (g_engine == 0) {  // the lean single-level kernel when the input fits its envelope (device or pinned host triplets)
     const int rc = sr::coo_to_csc<T, IdxT>(n_rows, n_cols, n, rows, cols, vals, mode, col_ptr, row_idx, out_vals, info,
                                            ws, ws_bytes, st);
     if (rc != -1) return rc;
@@ -65,6 +66,11 @@ static int coo_to_csc(long long n_rows, long long n_cols, long long n, const Idx
     return run_persist<T>(hs, NoSrc<T>{}, n_cols, row_bits, mode, 1, vs, col_ptr, row_idx, out_vals, info, true, ws,
                           pb, st);
   }
+  if (g_engine != 2) {  // large inputs: LSD bucket passes + the same tiles (largen.cuh)
+    const int rc = ln::coo_to_csc<T, IdxT>(n_rows, n_cols, n, rows, cols, vals, mode, col_ptr, row_idx, out_vals, info,
+                                           ws, ws_bytes, st);
+    if (rc != -1) return rc;
+  }
   ValSrc<T> vs{vals, nullptr, (unsigned long long)n};
   return run_persist<T>(s1, NoSrc<T>{}, n_cols, row_bits, mode, 1, vs, col_ptr, row_idx, out_vals, info, true, ws,
                         ws_bytes, st);
@@ -77,8 +83,13 @@ static int csc_transpose(long long n_rows, long long n_cols, long long nnz, cons
   AS_REQUIRE(n_rows >= 0 && n_cols >= 0 && n_rows <= kMaxDim && n_cols <= kMaxDim, AS_ERR_SHAPE,
              "dimensions %lldx%lld outside the int32 device index range", n_rows, n_cols);
   AS_REQUIRE(nnz >= 0 && nnz <= kMaxDim, AS_ERR_ARG, "nnz %lld outside the int32 range", nnz);
-  {
+  if (g_engine == 0) {
     const int rc = sr::transpose<T>(n_rows, n_cols, nnz, col_ptr, row_idx, vals, t_col_ptr, t_row_idx, t_vals, ws,
+                                    ws_bytes, st);
+    if (rc != -1) return rc;
+  }
+  if (g_engine != 2) {
+    const int rc = ln::transpose<T>(n_rows, n_cols, nnz, col_ptr, row_idx, vals, t_col_ptr, t_row_idx, t_vals, ws,
                                     ws_bytes, st);
     if (rc != -1) return rc;
   }
@@ -96,13 +107,14 @@ extern "C" {
 
 // (includes the staging of pinned-host triplets; a device-input build uses only the first part)
 size_t as_build_workspace_bytes(int64_t n, int64_t n_cols) {
-  return std::max(persist_ws_bytes(n, n_cols, 8) + staging_bytes(n, 8), sr::ws_bytes_api(n, 8));
+  return std::max({persist_ws_bytes(n, n_cols, 8) + staging_bytes(n, 8), sr::ws_bytes_api(n, 8),
+                   ln::ws_bytes(n, n_cols, 8)});
 }
 size_t as_flush_workspace_bytes(int64_t nnz_base, int64_t n_log, int64_t n_cols) {
   return std::max(persist_ws_bytes(nnz_base + n_log, n_cols, 8), sr::ws_bytes_api(nnz_base + n_log, 8));
 }
 size_t as_transpose_workspace_bytes(int64_t nnz, int64_t n_rows) {
-  return std::max(persist_ws_bytes(nnz, n_rows, 8), sr::ws_bytes_api(nnz, 8));
+  return std::max({persist_ws_bytes(nnz, n_rows, 8), sr::ws_bytes_api(nnz, 8), ln::ws_bytes(nnz, n_rows, 8)});
 }
 
 #define AS_BUILD_DISPATCH(T)                                                                                    \
@@ -135,7 +147,7 @@ int as_flush_log_f64(int64_t n_rows, int64_t n_cols, int64_t nnz_base, const int
              "dimensions %lldx%lld outside the int32 device index range", (long long)n_rows, (long long)n_cols);
   AS_REQUIRE(nnz_base >= 0 && n_log >= 0 && nnz_base + n_log <= kMaxDim, AS_ERR_ARG,
              "element count outside the int32 range");
-  {
+  if (g_engine == 0) {
     const int rc = sr::flush_f64(n_rows, n_cols, nnz_base, base_col_ptr, base_row_idx, base_vals, n_log, log_rows,
                                  log_cols, log_vals, col_ptr, row_idx, out_vals, (long long*)info, ws, ws_bytes,
                                  S(stream));

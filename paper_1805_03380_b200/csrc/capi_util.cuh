@@ -14,6 +14,7 @@
 namespace as {
 
 void set_error(const char* fmt, ...);
+extern int g_engine;  // as_set_engine: 0 auto, 1 large-input pipeline, 2 general bucket kernel
 
 #define AS_CUDA_TRY(expr)                                                        \
   do {                                                                           \

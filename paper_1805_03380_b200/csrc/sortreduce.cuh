@@ -520,7 +520,7 @@ AS_DEVICE_INLINE int bits_for_dev(long long maxval) {
 // Block-level stable LSD radix sort (8-bit digits) of (u64 key, u32 payload)
 // pairs in global memory, by the low idx_bits of the key, then key bits
 // [32, 32 + key_bits): (key32, input index) order.  Result in (k, p).
-__device__ void block_radix_sort_sr(unsigned long long* k, unsigned* p, unsigned long long* k_alt, unsigned* p_alt,
+__device__ inline void block_radix_sort_sr(unsigned long long* k, unsigned* p, unsigned long long* k_alt, unsigned* p_alt,
                                     long long L, int idx_bits, int key_bits, unsigned* hist, unsigned* wcnt) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kThreads / 32;
   unsigned long long *sk = k, *dk = k_alt;
@@ -595,18 +595,453 @@ __device__ void block_radix_sort_sr(unsigned long long* k, unsigned* p, unsigned
 // diagnostic step clocks (AS_PHASE_TIMES): CTA 0 records clock64 at step k
 #define SR_CLK(k, cond)                                                                                  \
   do {                                                                                                   \
-    if (kDbg && a.phase_ts && tid == 0 && (cond)) {                                                      \
+    if (kDbg && sr_dbg_ && tid == 0 && (cond)) {                                                           \
       const unsigned long long now_ = clock64();                                                         \
-      if (g == 0) a.phase_ts[8 + 3 * kMaxCb + (k)] = now_;                                               \
+      if (g == 0) sr_dbg_[8 + 3 * kMaxCb + (k)] = now_;                                                    \
       if ((k) <= 9) {                                                                                    \
         if ((k) > 0) {                                                                                   \
-          atomicAdd(&a.phase_ts[8 + 3 * kMaxCb + 32 + 2 * (k)], now_ - clk_prev_);                       \
-          atomicMax(&a.phase_ts[8 + 3 * kMaxCb + 33 + 2 * (k)], now_ - clk_prev_);                       \
+          atomicAdd(&sr_dbg_[8 + 3 * kMaxCb + 32 + 2 * (k)], now_ - clk_prev_);                            \
+          atomicMax(&sr_dbg_[8 + 3 * kMaxCb + 33 + 2 * (k)], now_ - clk_prev_);                            \
         }                                                                                                \
         clk_prev_ = now_;                                                                                \
       }                                                                                                  \
     }                                                                                                    \
   } while (0)
+
+// bucket t of the single-launch kernel = one run per chunk: run j at
+// gK[j * ch + loffT[t][j] ...]; prefix by the group look-back
+template <class T>
+struct SegSR {
+  const unsigned* loffT;
+  long long G, ch, ncb;
+  const unsigned* gK;
+  const unsigned* gX;
+  const T* gV;
+  unsigned long long* tstate;
+  const unsigned* cbcol;  // shared memory
+  __device__ __forceinline__ void seg(long long t, int tid, unsigned& len, unsigned& src) const {
+    if (tid < G) {
+      const unsigned s0 = __ldcg(&loffT[t * G + tid]), s1 = __ldcg(&loffT[(t + 1) * G + tid]);
+      len = s1 - s0;
+      src = (unsigned)(tid * ch) + s0;
+    }
+  }
+  __device__ __forceinline__ unsigned key(unsigned s) const { return __ldcg(&gK[s]); }
+  __device__ __forceinline__ unsigned idx(unsigned s) const { return __ldcg(&gX[s]); }
+  __device__ __forceinline__ const T* val(unsigned s) const { return gV + s; }
+  __device__ __forceinline__ unsigned col0(long long t) const { return cbcol[t]; }
+  __device__ __forceinline__ unsigned long long prefix(long long t, unsigned long long kept) const {
+    return group_lookback_warp(tstate, tstate + ncb, t, kept);
+  }
+};
+
+// ------------------------------------------------------------------------
+// The tile phase (P3 of the kernel below; also the last phase of the
+// large-input pipeline, largen.cuh): CTA-strided buckets t = t0, t0 + tstep,
+// ... < ncb.  A bucket of m <= kTile elements is loaded into registers /
+// shared memory, counting-sorted over <= kNB bins of its key range (bins never
+// straddle a column), every element ranks itself inside its bin by (key,
+// input index) (large bins: warp / block bitonic), runs of equal keys reduce
+// in the reference's order (np.add.reduceat pairwise, or last wins), exact
+// zeros are pruned, the kept count goes to the look-back, and rows / values /
+// col_ptr go straight to their final CSC positions.  A bucket above the tile
+// (a heavy column) is sorted by a block radix sort in global memory and
+// streamed (rare path).  `sg` names the bucket's elements: sg.seg (the runs
+// making up the bucket), sg.key / sg.idx / sg.val (bucket-local key, input
+// order, value address of a staging slot), sg.col0 (first column of a
+// bucket), sg.prefix (the look-back).  Both structs live in shared memory.
+template <class T>
+struct TileOut {
+  int mode, prune, mb, idx_bits, stop;
+  long long n_out_cols;
+  int* col_ptr;
+  int* row_idx;
+  T* out_vals;
+  long long* info;
+  unsigned long long* ctr1;  // oversized-bucket scratch allocator (zeroed before the phase)
+  unsigned long long* oK;
+  unsigned long long* oK2;
+  unsigned* oP;
+  unsigned* oP2;
+  int* oR;
+  T* oV;
+  unsigned long long* phase_ts;
+};
+
+template <class T, class Seg>
+__device__ __forceinline__ void tile_phase(const Seg& sg, const TileOut<T>& o, TileSmem<T>& S, long long t0,
+                                           long long tstep, long long ncb) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long g = blockIdx.x;
+  const int mb = o.mb;
+  unsigned long long clk_prev_ = 0;
+  unsigned long long* const sr_dbg_ = o.phase_ts;
+  (void)clk_prev_;
+  (void)g;
+  (void)sr_dbg_;
+  for (int b = tid; b < kNB; b += kThreads) S.cnt[b] = 0u;
+  const unsigned mmask = mb >= 32 ? 0xffffffffu : ((1u << mb) - 1u);
+  for (long long t = t0; t < ncb; t += tstep) {
+    const unsigned col_base = sg.col0(t);
+    const int Wt = (int)(sg.col0(t + 1) - col_base);
+    // bucket t = one run per chunk: run j at gK[j * ch + loffT[t][j] ...]
+    unsigned seglen = 0, segsrc = 0;
+    sg.seg(t, tid, seglen, segsrc);
+    __syncthreads();  // the previous tile's shared memory is free; cnt zeroed
+    unsigned m_u;
+    const unsigned segoff = block_scan_u32(seglen, S.scan32, &m_u);
+    const int m = (int)m_u;
+    auto lookback = [&](long long kept) -> long long {
+      if (kDbg && o.phase_ts && tid == 0) o.phase_ts[8 + 3 * t] = global_ns();
+      if (tid < 32) {
+        const unsigned long long pre = sg.prefix(t, (unsigned long long)kept);
+        if (tid == 0) S.prefix = (long long)pre;
+      }
+      __syncthreads();
+      if (kDbg && o.phase_ts && tid == 0) o.phase_ts[8 + 3 * t + 1] = global_ns();
+      const long long base = S.prefix;
+      if (t == ncb - 1 && tid == 0) {
+        o.col_ptr[o.n_out_cols] = (int)(base + kept);
+        o.info[0] = base + kept;
+      }
+      return base;
+    };
+    if (m == 0) {
+      const long long base = lookback(0);
+      for (int l = tid; l < Wt; l += kThreads) o.col_ptr[col_base + l] = (int)base;
+      continue;
+    }
+    if (__builtin_expect(m > kTile, 0)) {
+      // ---------- oversized bucket (rare): global-memory radix sort ----------
+      if (tid == 0) S.prefix = (long long)atomicAdd(o.ctr1, (unsigned long long)m);  // scratch range
+      __syncthreads();
+      const long long s = S.prefix;
+      unsigned long long* K1 = o.oK + s;
+      unsigned long long* K2 = o.oK2 + s;
+      unsigned* P1 = o.oP + s;
+      unsigned* P2 = o.oP2 + s;
+      for (unsigned e = 0; e < seglen; e++) {  // gather the runs (payload: staging slot of the value)
+        K1[segoff + e] = ((unsigned long long)sg.key(segsrc + e) << 32) | sg.idx(segsrc + e);
+        P1[segoff + e] = segsrc + e;
+      }
+      for (int l = tid; l < Wt; l += kThreads) S.u.r.ckept[l] = 0u;
+      __syncthreads();
+      block_radix_sort_sr(K1, P1, K2, P2, m, o.idx_bits, mb + bits_for_dev(Wt > 0 ? Wt - 1 : 0), S.u.r.hist,
+                          S.u.r.wcnt);
+      auto gv = [&](unsigned s) -> T { return *sg.val(s); };
+      long long running = 0;
+      for (int base0 = 0; base0 < m; base0 += kThreads) {
+        const int p = base0 + tid;
+        bool kept = false, longrun = false;
+        T v = T(0);
+        unsigned k = 0;
+        long long rl = 0;
+        if (p < m) {
+          k = (unsigned)(K1[p] >> 32);
+          const bool head = p == 0 || (unsigned)(K1[p - 1] >> 32) != k;
+          if (head) {
+            int q = p + 1;
+            while (q < m && (unsigned)(K1[q] >> 32) == k) q++;
+            rl = q - p;
+            if (o.mode == kLast) {
+              v = gv(P1[q - 1]);
+            } else if (rl == 1) {
+              v = gv(P1[p]);
+            } else {
+              longrun = true;
+            }
+            kept = !longrun && (!o.prune || v != T(0));
+          }
+        }
+        for (unsigned lm = __ballot_sync(0xffffffffu, longrun); lm; lm &= lm - 1) {
+          if (lane == __ffs(lm) - 1) {
+            const unsigned* pp = P1 + p + 1;
+            v = gv(P1[p]) + pw_stack<T>([&](int i) -> T { return gv(pp[i]); }, (int)(rl - 1), S.wst[warp]);
+            kept = !o.prune || v != T(0);
+          }
+          __syncwarp();
+        }
+        long long tot;
+        const long long off = block_exclusive_scan<long long>(kept ? 1ll : 0ll, S.scan, &tot);
+        if (kept) {
+          o.oR[s + running + off] = (int)(k & mmask);
+          o.oV[s + running + off] = v;
+          atomicAdd(&S.u.r.ckept[k >> mb], 1u);
+        }
+        running += tot;
+      }
+      __syncthreads();
+      const long long base = lookback(running);
+      for (long long i = tid; i < running; i += kThreads) {
+        o.row_idx[base + i] = __ldcg(&o.oR[s + i]);
+        o.out_vals[base + i] = __ldcg(&o.oV[s + i]);
+      }
+      long long run = base;
+      for (int l0 = 0; l0 < Wt; l0 += kThreads) {
+        const int l = l0 + tid;
+        long long tot;
+        const long long ex = block_exclusive_scan<long long>(l < Wt ? (long long)S.u.r.ckept[l] : 0ll, S.scan, &tot);
+        if (l < Wt) o.col_ptr[col_base + l] = (int)(run + ex);
+        run += tot;
+      }
+      continue;
+    }
+
+    // ---------- tile ----------
+    // element i = tid + u * kThreads (striped: a warp's shared-memory accesses
+    // are consecutive wherever the layout allows); bins: aligned ranges of the
+    // key between 0 and Wt << mb, at most kNB, never wider than one column
+    SR_CLK(0, t == g);
+    const unsigned long long range = (unsigned long long)Wt << mb;
+    int sh = 0;
+    while (((range - 1) >> sh) >= (unsigned long long)kNB) sh++;
+    const int nbins = (int)(((range - 1) >> sh) + 1);
+    // staging slot of every element of the tile (the map aliases TK, written later)
+    for (unsigned e = 0; e < seglen; e++) S.u.a.TK[segoff + e] = segsrc + e;
+    __syncthreads();
+    unsigned k4[kTP], x4[kTP], br[kTP];
+#pragma unroll
+    for (int u = 0; u < kTP; u++) {
+      const int i = tid + u * kThreads;
+      if (i < m) {
+        const unsigned src = S.u.a.TK[i];
+        k4[u] = sg.key(src);
+        x4[u] = sg.idx(src);
+        const unsigned d = (unsigned)__cvta_generic_to_shared(&S.u.a.V[i]);
+        if constexpr (sizeof(T) == 8)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(sg.val(src)) : "memory");
+        else
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(sg.val(src)) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    SR_CLK(1, t == g);
+    if (kDbg && o.phase_ts && tid == 0) o.phase_ts[8 + 3 * t + 2] = global_ns();
+#pragma unroll
+    for (int u = 0; u < kTP; u++) {
+      if (tid + u * kThreads < m) {
+        const unsigned b = k4[u] >> sh;
+        br[u] = (b << 16) | atomicAdd(&S.cnt[b], 1u);
+      }
+    }
+    if (tid == 0) S.n_big = 0;
+    asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's values landed
+    __syncthreads();
+    SR_CLK(2, t == g);
+    if (kDbg && o.stop == 3) return;
+    {  // bin starts (kNB / kThreads consecutive bins per thread); counts re-zeroed
+      constexpr int kB = kNB / kThreads;
+      const int b0 = tid * kB;
+      unsigned c[kB], sum = 0;
+#pragma unroll
+      for (int q = 0; q < kB; q++) {
+        c[q] = b0 + q < nbins ? S.cnt[b0 + q] : 0u;
+        sum += c[q];
+      }
+      unsigned tot;
+      unsigned run = block_scan_u32(sum, S.scan32, &tot);
+#pragma unroll
+      for (int q = 0; q < kB; q++) {
+        if (b0 + q < nbins) {
+          S.bs[b0 + q] = run;
+          S.cnt[b0 + q] = 0u;
+          if (c[q] > kRankMax) S.big[atomicAdd(&S.n_big, 1)] = (unsigned short)(b0 + q);
+        }
+        run += c[q];
+      }
+      if (tid == 0) S.bs[nbins] = (unsigned)m;
+    }
+    __syncthreads();
+    SR_CLK(3, t == g);
+    if (kDbg && o.stop == 7) return;
+#pragma unroll
+    for (int u = 0; u < kTP; u++) {
+      if (tid + u * kThreads < m) {
+        const unsigned pos = S.bs[br[u] >> 16] + (br[u] & 0xffffu);
+        S.u.a.TK[pos] = k4[u];
+        S.u.a.TX[pos] = x4[u];
+      }
+    }
+    for (int l = tid; l <= Wt; l += kThreads) {
+      const unsigned long long bl = ((unsigned long long)l << mb) >> sh;
+      S.cstart[l] = (unsigned short)S.bs[bl < (unsigned long long)nbins ? bl : nbins];
+    }
+    __syncthreads();
+    SR_CLK(4, t == g);
+    if (kDbg && o.stop == 8) return;
+    // each element ranks itself inside its bin by (key, input index): final position
+#pragma unroll
+    for (int u = 0; u < kTP; u++) {
+      const int i = tid + u * kThreads;
+      if (i < m) {
+        const unsigned b = br[u] >> 16;
+        const unsigned b0 = S.bs[b], b1 = S.bs[b + 1];
+        if (b1 - b0 <= kRankMax) {
+          // branch-free count of the bin's (key, index) pairs below this one
+          unsigned r = 0;
+          const unsigned k = k4[u], x = x4[u];
+          for (unsigned j = b0; j < b1; j++) {
+            const unsigned kj = S.u.a.TK[j], xj = S.u.a.TX[j];
+            r += (unsigned)(kj < k) | ((unsigned)(kj == k) & (unsigned)(xj < x));
+          }
+          S.SK[b0 + r] = k;
+          S.SI[b0 + r] = (unsigned short)i;
+        }
+      }
+    }
+    const int n_big = S.n_big;
+    if (kDbg && o.phase_ts && tid == 0 && n_big) atomicAdd(&o.phase_ts[5], (unsigned long long)n_big);
+    if (__builtin_expect(n_big != 0, 0)) {  // bins above kRankMax (rare): warp bitonic (<= 512), block bitonic beyond
+      for (int q = warp; q < n_big; q += kThreads / 32) {
+        const int b = S.big[q];
+        const int b0 = S.bs[b], L = S.bs[b + 1] - b0;
+        if (L > 512) continue;
+        for (int j = lane; j < L; j += 32) S.u.a.BK[b0 + j] = ((unsigned long long)S.u.a.TK[b0 + j] << 32) | S.u.a.TX[b0 + j];
+        __syncwarp();
+        bitonic_sort<false>(S.u.a.BK + b0, L, lane, 32);
+        for (int j = lane; j < L; j += 32) S.SK[b0 + j] = (unsigned)(S.u.a.BK[b0 + j] >> 32);
+      }
+      __syncthreads();
+      for (int q = 0; q < n_big; q++) {
+        const int b = S.big[q];
+        const int b0 = S.bs[b], L = S.bs[b + 1] - b0;
+        if (L <= 512) continue;
+        for (int j = tid; j < L; j += kThreads) S.u.a.BK[b0 + j] = ((unsigned long long)S.u.a.TK[b0 + j] << 32) | S.u.a.TX[b0 + j];
+        __syncthreads();
+        bitonic_sort<true>(S.u.a.BK + b0, L, tid, kThreads);
+        for (int j = tid; j < L; j += kThreads) S.SK[b0 + j] = (unsigned)(S.u.a.BK[b0 + j] >> 32);
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+    if (__builtin_expect(n_big != 0, 0)) {  // the sorted (key, index) pairs of big bins name their elements by input index
+#pragma unroll
+      for (int u = 0; u < kTP; u++) {
+        const int i = tid + u * kThreads;
+        if (i < m) {
+          const unsigned b = br[u] >> 16;
+          const unsigned b0 = S.bs[b], b1 = S.bs[b + 1];
+          if (b1 - b0 > kRankMax) {  // find this element's (key, index) in the sorted bin
+            const unsigned long long kx = ((unsigned long long)k4[u] << 32) | x4[u];
+            unsigned lo2 = b0, hi2 = b1;
+            while (lo2 < hi2) {
+              const unsigned mid = (lo2 + hi2) >> 1;
+              if (S.u.a.BK[mid] < kx) lo2 = mid + 1;
+              else hi2 = mid;
+            }
+            S.SI[lo2] = (unsigned short)i;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    SR_CLK(5, t == g);
+    if (kDbg && o.stop == 4) return;
+    // runs (striped positions p = tid + u * kThreads): a run belongs to its
+    // head, whose value goes to RV[head]; runs of several values are summed
+    // in one non-unrolled loop (a single copy of the pairwise code), the
+    // ones above one pairwise leaf with the warp's stack one lane at a time
+    unsigned hmask = 0, multi = 0;
+#pragma unroll
+    for (int u = 0; u < kTP; u++) {
+      const int p = tid + u * kThreads;
+      if (p < m) {
+        const unsigned k = S.SK[p];
+        if (p == 0 || S.SK[p - 1] != k) {
+          hmask |= 1u << u;
+          if (p + 1 < m && S.SK[p + 1] == k) {
+            multi |= 1u << u;
+          } else {
+            S.u.a.RV[p] = S.u.a.V[S.SI[p]];
+          }
+        }
+      }
+    }
+    if (o.mode == kLast) {
+#pragma unroll 1
+      for (int u = 0; u < kTP; u++) {
+        if (!(multi >> u & 1u)) continue;
+        const int p = tid + u * kThreads;
+        const unsigned k = S.SK[p];
+        int q = p + 2;
+        while (q < m && S.SK[q] == k) q++;
+        S.u.a.RV[p] = S.u.a.V[S.SI[q - 1]];
+      }
+      multi = 0;
+    }
+    // Sum runs of several values (pairwise order, np.add.reduceat): the
+    // warp's lanes one at a time, sharing the warp's stack (rare: duplicates)
+    for (unsigned lm = __ballot_sync(0xffffffffu, multi != 0); __builtin_expect(lm != 0, 0); lm &= lm - 1) {
+      if (lane == __ffs(lm) - 1) {
+#pragma unroll 1
+        for (int u = 0; u < kTP; u++) {
+          if (!(multi >> u & 1u)) continue;
+          const int p = tid + u * kThreads;
+          const unsigned k = S.SK[p];
+          int q = p + 2;
+          while (q < m && S.SK[q] == k) q++;
+          const unsigned short* si = S.SI + p + 1;
+          S.u.a.RV[p] = S.u.a.V[S.SI[p]] + pw_stack<T>([&](int j) -> T { return S.u.a.V[si[j]]; }, q - p - 1,
+                                                        S.wst[warp]);
+        }
+      }
+      __syncwarp();
+    }
+    bool kp[kTP];
+#pragma unroll
+    for (int u = 0; u < kTP; u++) {
+      const int p = tid + u * kThreads;
+      kp[u] = (hmask >> u & 1u) && (!o.prune || S.u.a.RV[p] != T(0));
+      const unsigned w = __ballot_sync(0xffffffffu, kp[u]);
+      if (lane == 0) S.kw[u * (kThreads / 32) + warp] = w;
+    }
+    SR_CLK(6, t == g);
+    __syncthreads();
+    long long total = 0;
+    if (warp == 0) {  // prefix over the kTile / 32 words
+      constexpr int kW = kTile / 32;
+      unsigned c[kW / 32], sum = 0;
+#pragma unroll
+      for (int q = 0; q < kW / 32; q++) {
+        c[q] = __popc(S.kw[lane * (kW / 32) + q]);
+        sum += c[q];
+      }
+      const unsigned inc = warp_inclusive_scan(sum);
+      unsigned run = inc - sum;
+#pragma unroll
+      for (int q = 0; q < kW / 32; q++) {
+        S.kwp[lane * (kW / 32) + q] = run;
+        run += c[q];
+      }
+      if (lane == 31) S.kwp[kW] = inc;
+    }
+    __syncthreads();
+    total = S.kwp[kTile / 32];
+    SR_CLK(7, t == g);
+    if (kDbg && o.stop == 5) return;
+    const long long base = lookback(total);
+    SR_CLK(8, t == g);
+    if (kDbg && o.stop == 6) return;
+#pragma unroll
+    for (int u = 0; u < kTP; u++) {
+      if (kp[u]) {
+        const int p = tid + u * kThreads;
+        const int w = p >> 5;
+        const long long e = base + S.kwp[w] + __popc(S.kw[w] & lanemask_lt());
+        __stcs(&o.row_idx[e], (int)(S.SK[p] & mmask));
+        __stcs(&o.out_vals[e], S.u.a.RV[p]);
+      }
+    }
+    for (int l = tid; l < Wt; l += kThreads) {
+      const int p = S.cstart[l];
+      const int w = p >> 5;
+      const unsigned e = p >= m ? (unsigned)total : S.kwp[w] + __popc(S.kw[w] & ((1u << (p & 31)) - 1u));
+      o.col_ptr[col_base + l] = (int)(base + e);
+    }
+    SR_CLK(9, t == g);
+  }
+}
+
 
 // ------------------------------------------------------------------------
 template <class T, class S1, class S2>
@@ -632,6 +1067,7 @@ __global__ void __launch_bounds__(kThreads, 2) sortreduce_kernel(Args<T, S1, S2>
   const unsigned long long cb_mul = a.cb_mul;
   const int mb = a.minor_bits;
   unsigned long long clk_prev_ = 0;
+  unsigned long long* const sr_dbg_ = a.phase_ts;
   if (kDbg && a.phase_ts && tid == 0) {
     const unsigned long long t0 = global_ns();
     atomicMin(&a.phase_ts[0], t0);
@@ -775,371 +1211,39 @@ __global__ void __launch_bounds__(kThreads, 2) sortreduce_kernel(Args<T, S1, S2>
 
   // ---------------- P3 ----------------
   TileSmem<T>& S = *reinterpret_cast<TileSmem<T>*>(smem + LY.tile_off);
-  for (int b = tid; b < kNB; b += kThreads) S.cnt[b] = 0u;
-  const unsigned mmask = mb >= 32 ? 0xffffffffu : ((1u << mb) - 1u);
-  for (long long t = g; t < ncb; t += G) {
-    const unsigned col_base = cbcol[t];
-    const int Wt = (int)(cbcol[t + 1] - col_base);
-    // bucket t = one run per chunk: run j at gK[j * ch + loffT[t][j] ...]
-    unsigned seglen = 0, segsrc = 0;
-    if (tid < G) {
-      const unsigned s0 = __ldcg(&a.loffT[t * G + tid]), s1 = __ldcg(&a.loffT[(t + 1) * G + tid]);
-      seglen = s1 - s0;
-      segsrc = (unsigned)(tid * a.ch) + s0;
-    }
-    __syncthreads();  // the previous tile's shared memory is free; cnt zeroed
-    unsigned m_u;
-    const unsigned segoff = block_scan_u32(seglen, S.scan32, &m_u);
-    const int m = (int)m_u;
-    auto lookback = [&](long long kept) -> long long {
-      if (kDbg && a.phase_ts && tid == 0) a.phase_ts[8 + 3 * t] = global_ns();
-      if (tid < 32) {
-        const unsigned long long pre = group_lookback_warp(a.tstate, a.tstate + ncb, t, (unsigned long long)kept);
-        if (tid == 0) S.prefix = (long long)pre;
-      }
-      __syncthreads();
-      if (kDbg && a.phase_ts && tid == 0) a.phase_ts[8 + 3 * t + 1] = global_ns();
-      const long long base = S.prefix;
-      if (t == ncb - 1 && tid == 0) {
-        a.col_ptr[a.n_out_cols] = (int)(base + kept);
-        a.info[0] = base + kept;
-      }
-      return base;
-    };
-    if (m == 0) {
-      const long long base = lookback(0);
-      for (int l = tid; l < Wt; l += kThreads) a.col_ptr[col_base + l] = (int)base;
-      continue;
-    }
-    if (__builtin_expect(m > kTile, 0)) {
-      // ---------- oversized bucket (rare): global-memory radix sort ----------
-      if (tid == 0) S.prefix = (long long)atomicAdd(&a.ctr[1], (unsigned long long)m);  // scratch range
-      __syncthreads();
-      const long long s = S.prefix;
-      unsigned long long* K1 = a.oK + s;
-      unsigned long long* K2 = a.oK2 + s;
-      unsigned* P1 = a.oP + s;
-      unsigned* P2 = a.oP2 + s;
-      for (unsigned e = 0; e < seglen; e++) {  // gather the runs (payload: staging slot of the value)
-        K1[segoff + e] = ((unsigned long long)__ldcg(&a.gK[segsrc + e]) << 32) | __ldcg(&a.gX[segsrc + e]);
-        P1[segoff + e] = segsrc + e;
-      }
-      for (int l = tid; l < Wt; l += kThreads) S.u.r.ckept[l] = 0u;
-      __syncthreads();
-      block_radix_sort_sr(K1, P1, K2, P2, m, a.idx_bits, mb + bits_for_dev(Wt > 0 ? Wt - 1 : 0), S.u.r.hist,
-                          S.u.r.wcnt);
-      const T* gv = a.gV;
-      long long running = 0;
-      for (int base0 = 0; base0 < m; base0 += kThreads) {
-        const int p = base0 + tid;
-        bool kept = false, longrun = false;
-        T v = T(0);
-        unsigned k = 0;
-        long long rl = 0;
-        if (p < m) {
-          k = (unsigned)(K1[p] >> 32);
-          const bool head = p == 0 || (unsigned)(K1[p - 1] >> 32) != k;
-          if (head) {
-            int q = p + 1;
-            while (q < m && (unsigned)(K1[q] >> 32) == k) q++;
-            rl = q - p;
-            if (a.mode == kLast) {
-              v = gv[P1[q - 1]];
-            } else if (rl == 1) {
-              v = gv[P1[p]];
-            } else {
-              longrun = true;
-            }
-            kept = !longrun && (!a.prune || v != T(0));
-          }
-        }
-        for (unsigned lm = __ballot_sync(0xffffffffu, longrun); lm; lm &= lm - 1) {
-          if (lane == __ffs(lm) - 1) {
-            const unsigned* pp = P1 + p + 1;
-            v = gv[P1[p]] + pw_stack<T>([&](int i) -> T { return gv[pp[i]]; }, (int)(rl - 1), S.wst[warp]);
-            kept = !a.prune || v != T(0);
-          }
-          __syncwarp();
-        }
-        long long tot;
-        const long long off = block_exclusive_scan<long long>(kept ? 1ll : 0ll, S.scan, &tot);
-        if (kept) {
-          a.oR[s + running + off] = (int)(k & mmask);
-          a.oV[s + running + off] = v;
-          atomicAdd(&S.u.r.ckept[k >> mb], 1u);
-        }
-        running += tot;
-      }
-      __syncthreads();
-      const long long base = lookback(running);
-      for (long long i = tid; i < running; i += kThreads) {
-        a.row_idx[base + i] = __ldcg(&a.oR[s + i]);
-        a.out_vals[base + i] = __ldcg(&a.oV[s + i]);
-      }
-      long long run = base;
-      for (int l0 = 0; l0 < Wt; l0 += kThreads) {
-        const int l = l0 + tid;
-        long long tot;
-        const long long ex = block_exclusive_scan<long long>(l < Wt ? (long long)S.u.r.ckept[l] : 0ll, S.scan, &tot);
-        if (l < Wt) a.col_ptr[col_base + l] = (int)(run + ex);
-        run += tot;
-      }
-      continue;
-    }
-
-    // ---------- tile ----------
-    // element i = tid + u * kThreads (striped: a warp's shared-memory accesses
-    // are consecutive wherever the layout allows); bins: aligned ranges of the
-    // key between 0 and Wt << mb, at most kNB, never wider than one column
-    SR_CLK(0, t == g);
-    const unsigned long long range = (unsigned long long)Wt << mb;
-    int sh = 0;
-    while (((range - 1) >> sh) >= (unsigned long long)kNB) sh++;
-    const int nbins = (int)(((range - 1) >> sh) + 1);
-    // staging slot of every element of the tile (the map aliases TK, written later)
-    for (unsigned e = 0; e < seglen; e++) S.u.a.TK[segoff + e] = segsrc + e;
-    __syncthreads();
-    unsigned k4[kTP], x4[kTP], br[kTP];
-#pragma unroll
-    for (int u = 0; u < kTP; u++) {
-      const int i = tid + u * kThreads;
-      if (i < m) {
-        const unsigned src = S.u.a.TK[i];
-        k4[u] = __ldcg(&a.gK[src]);
-        x4[u] = __ldcg(&a.gX[src]);
-        const unsigned d = (unsigned)__cvta_generic_to_shared(&S.u.a.V[i]);
-        if constexpr (sizeof(T) == 8)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(a.gV + src) : "memory");
-        else
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(a.gV + src) : "memory");
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    SR_CLK(1, t == g);
-    if (kDbg && a.phase_ts && tid == 0) a.phase_ts[8 + 3 * t + 2] = global_ns();
-#pragma unroll
-    for (int u = 0; u < kTP; u++) {
-      if (tid + u * kThreads < m) {
-        const unsigned b = k4[u] >> sh;
-        br[u] = (b << 16) | atomicAdd(&S.cnt[b], 1u);
-      }
-    }
-    if (tid == 0) S.n_big = 0;
-    asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's values landed
-    __syncthreads();
-    SR_CLK(2, t == g);
-    if (kDbg && a.stop == 3) return;
-    {  // bin starts (kNB / kThreads consecutive bins per thread); counts re-zeroed
-      constexpr int kB = kNB / kThreads;
-      const int b0 = tid * kB;
-      unsigned c[kB], sum = 0;
-#pragma unroll
-      for (int q = 0; q < kB; q++) {
-        c[q] = b0 + q < nbins ? S.cnt[b0 + q] : 0u;
-        sum += c[q];
-      }
-      unsigned tot;
-      unsigned run = block_scan_u32(sum, S.scan32, &tot);
-#pragma unroll
-      for (int q = 0; q < kB; q++) {
-        if (b0 + q < nbins) {
-          S.bs[b0 + q] = run;
-          S.cnt[b0 + q] = 0u;
-          if (c[q] > kRankMax) S.big[atomicAdd(&S.n_big, 1)] = (unsigned short)(b0 + q);
-        }
-        run += c[q];
-      }
-      if (tid == 0) S.bs[nbins] = (unsigned)m;
-    }
-    __syncthreads();
-    SR_CLK(3, t == g);
-    if (kDbg && a.stop == 7) return;
-#pragma unroll
-    for (int u = 0; u < kTP; u++) {
-      if (tid + u * kThreads < m) {
-        const unsigned pos = S.bs[br[u] >> 16] + (br[u] & 0xffffu);
-        S.u.a.TK[pos] = k4[u];
-        S.u.a.TX[pos] = x4[u];
-      }
-    }
-    for (int l = tid; l <= Wt; l += kThreads) {
-      const unsigned long long bl = ((unsigned long long)l << mb) >> sh;
-      S.cstart[l] = (unsigned short)S.bs[bl < (unsigned long long)nbins ? bl : nbins];
-    }
-    __syncthreads();
-    SR_CLK(4, t == g);
-    if (kDbg && a.stop == 8) return;
-    // each element ranks itself inside its bin by (key, input index): final position
-#pragma unroll
-    for (int u = 0; u < kTP; u++) {
-      const int i = tid + u * kThreads;
-      if (i < m) {
-        const unsigned b = br[u] >> 16;
-        const unsigned b0 = S.bs[b], b1 = S.bs[b + 1];
-        if (b1 - b0 <= kRankMax) {
-          // branch-free count of the bin's (key, index) pairs below this one
-          unsigned r = 0;
-          const unsigned k = k4[u], x = x4[u];
-          for (unsigned j = b0; j < b1; j++) {
-            const unsigned kj = S.u.a.TK[j], xj = S.u.a.TX[j];
-            r += (unsigned)(kj < k) | ((unsigned)(kj == k) & (unsigned)(xj < x));
-          }
-          S.SK[b0 + r] = k;
-          S.SI[b0 + r] = (unsigned short)i;
-        }
-      }
-    }
-    const int n_big = S.n_big;
-    if (kDbg && a.phase_ts && tid == 0 && n_big) atomicAdd(&a.phase_ts[5], (unsigned long long)n_big);
-    if (__builtin_expect(n_big != 0, 0)) {  // bins above kRankMax (rare): warp bitonic (<= 512), block bitonic beyond
-      for (int q = warp; q < n_big; q += kThreads / 32) {
-        const int b = S.big[q];
-        const int b0 = S.bs[b], L = S.bs[b + 1] - b0;
-        if (L > 512) continue;
-        for (int j = lane; j < L; j += 32) S.u.a.BK[b0 + j] = ((unsigned long long)S.u.a.TK[b0 + j] << 32) | S.u.a.TX[b0 + j];
-        __syncwarp();
-        bitonic_sort<false>(S.u.a.BK + b0, L, lane, 32);
-        for (int j = lane; j < L; j += 32) S.SK[b0 + j] = (unsigned)(S.u.a.BK[b0 + j] >> 32);
-      }
-      __syncthreads();
-      for (int q = 0; q < n_big; q++) {
-        const int b = S.big[q];
-        const int b0 = S.bs[b], L = S.bs[b + 1] - b0;
-        if (L <= 512) continue;
-        for (int j = tid; j < L; j += kThreads) S.u.a.BK[b0 + j] = ((unsigned long long)S.u.a.TK[b0 + j] << 32) | S.u.a.TX[b0 + j];
-        __syncthreads();
-        bitonic_sort<true>(S.u.a.BK + b0, L, tid, kThreads);
-        for (int j = tid; j < L; j += kThreads) S.SK[b0 + j] = (unsigned)(S.u.a.BK[b0 + j] >> 32);
-        __syncthreads();
-      }
-    }
-    __syncthreads();
-    if (__builtin_expect(n_big != 0, 0)) {  // the sorted (key, index) pairs of big bins name their elements by input index
-#pragma unroll
-      for (int u = 0; u < kTP; u++) {
-        const int i = tid + u * kThreads;
-        if (i < m) {
-          const unsigned b = br[u] >> 16;
-          const unsigned b0 = S.bs[b], b1 = S.bs[b + 1];
-          if (b1 - b0 > kRankMax) {  // find this element's (key, index) in the sorted bin
-            const unsigned long long kx = ((unsigned long long)k4[u] << 32) | x4[u];
-            unsigned lo2 = b0, hi2 = b1;
-            while (lo2 < hi2) {
-              const unsigned mid = (lo2 + hi2) >> 1;
-              if (S.u.a.BK[mid] < kx) lo2 = mid + 1;
-              else hi2 = mid;
-            }
-            S.SI[lo2] = (unsigned short)i;
-          }
-        }
-      }
-      __syncthreads();
-    }
-    SR_CLK(5, t == g);
-    if (kDbg && a.stop == 4) return;
-    // runs (striped positions p = tid + u * kThreads): a run belongs to its
-    // head, whose value goes to RV[head]; runs of several values are summed
-    // in one non-unrolled loop (a single copy of the pairwise code), the
-    // ones above one pairwise leaf with the warp's stack one lane at a time
-    unsigned hmask = 0, multi = 0;
-#pragma unroll
-    for (int u = 0; u < kTP; u++) {
-      const int p = tid + u * kThreads;
-      if (p < m) {
-        const unsigned k = S.SK[p];
-        if (p == 0 || S.SK[p - 1] != k) {
-          hmask |= 1u << u;
-          if (p + 1 < m && S.SK[p + 1] == k) {
-            multi |= 1u << u;
-          } else {
-            S.u.a.RV[p] = S.u.a.V[S.SI[p]];
-          }
-        }
-      }
-    }
-    if (a.mode == kLast) {
-#pragma unroll 1
-      for (int u = 0; u < kTP; u++) {
-        if (!(multi >> u & 1u)) continue;
-        const int p = tid + u * kThreads;
-        const unsigned k = S.SK[p];
-        int q = p + 2;
-        while (q < m && S.SK[q] == k) q++;
-        S.u.a.RV[p] = S.u.a.V[S.SI[q - 1]];
-      }
-      multi = 0;
-    }
-    // Sum runs of several values (pairwise order, np.add.reduceat): the
-    // warp's lanes one at a time, sharing the warp's stack (rare: duplicates)
-    for (unsigned lm = __ballot_sync(0xffffffffu, multi != 0); __builtin_expect(lm != 0, 0); lm &= lm - 1) {
-      if (lane == __ffs(lm) - 1) {
-#pragma unroll 1
-        for (int u = 0; u < kTP; u++) {
-          if (!(multi >> u & 1u)) continue;
-          const int p = tid + u * kThreads;
-          const unsigned k = S.SK[p];
-          int q = p + 2;
-          while (q < m && S.SK[q] == k) q++;
-          const unsigned short* si = S.SI + p + 1;
-          S.u.a.RV[p] = S.u.a.V[S.SI[p]] + pw_stack<T>([&](int j) -> T { return S.u.a.V[si[j]]; }, q - p - 1,
-                                                        S.wst[warp]);
-        }
-      }
-      __syncwarp();
-    }
-    bool kp[kTP];
-#pragma unroll
-    for (int u = 0; u < kTP; u++) {
-      const int p = tid + u * kThreads;
-      kp[u] = (hmask >> u & 1u) && (!a.prune || S.u.a.RV[p] != T(0));
-      const unsigned w = __ballot_sync(0xffffffffu, kp[u]);
-      if (lane == 0) S.kw[u * (kThreads / 32) + warp] = w;
-    }
-    SR_CLK(6, t == g);
-    __syncthreads();
-    long long total = 0;
-    if (warp == 0) {  // prefix over the kTile / 32 words
-      constexpr int kW = kTile / 32;
-      unsigned c[kW / 32], sum = 0;
-#pragma unroll
-      for (int q = 0; q < kW / 32; q++) {
-        c[q] = __popc(S.kw[lane * (kW / 32) + q]);
-        sum += c[q];
-      }
-      const unsigned inc = warp_inclusive_scan(sum);
-      unsigned run = inc - sum;
-#pragma unroll
-      for (int q = 0; q < kW / 32; q++) {
-        S.kwp[lane * (kW / 32) + q] = run;
-        run += c[q];
-      }
-      if (lane == 31) S.kwp[kW] = inc;
-    }
-    __syncthreads();
-    total = S.kwp[kTile / 32];
-    SR_CLK(7, t == g);
-    if (kDbg && a.stop == 5) return;
-    const long long base = lookback(total);
-    SR_CLK(8, t == g);
-    if (kDbg && a.stop == 6) return;
-#pragma unroll
-    for (int u = 0; u < kTP; u++) {
-      if (kp[u]) {
-        const int p = tid + u * kThreads;
-        const int w = p >> 5;
-        const long long e = base + S.kwp[w] + __popc(S.kw[w] & lanemask_lt());
-        __stcs(&a.row_idx[e], (int)(S.SK[p] & mmask));
-        __stcs(&a.out_vals[e], S.u.a.RV[p]);
-      }
-    }
-    for (int l = tid; l < Wt; l += kThreads) {
-      const int p = S.cstart[l];
-      const int w = p >> 5;
-      const unsigned e = p >= m ? (unsigned)total : S.kwp[w] + __popc(S.kw[w] & ((1u << (p & 31)) - 1u));
-      a.col_ptr[col_base + l] = (int)(base + e);
-    }
-    SR_CLK(9, t == g);
+  __shared__ TileOut<T> to;
+  __shared__ SegSR<T> sgs;
+  if (tid == 0) {
+    to.mode = a.mode;
+    to.prune = a.prune;
+    to.mb = a.minor_bits;
+    to.idx_bits = a.idx_bits;
+    to.stop = a.stop;
+    to.n_out_cols = a.n_out_cols;
+    to.col_ptr = a.col_ptr;
+    to.row_idx = a.row_idx;
+    to.out_vals = a.out_vals;
+    to.info = a.info;
+    to.ctr1 = a.ctr + 1;
+    to.oK = a.oK;
+    to.oK2 = a.oK2;
+    to.oP = a.oP;
+    to.oP2 = a.oP2;
+    to.oR = a.oR;
+    to.oV = a.oV;
+    to.phase_ts = a.phase_ts;
+    sgs.loffT = a.loffT;
+    sgs.G = G;
+    sgs.ch = a.ch;
+    sgs.ncb = ncb;
+    sgs.gK = a.gK;
+    sgs.gX = a.gX;
+    sgs.gV = a.gV;
+    sgs.tstate = a.tstate;
+    sgs.cbcol = cbcol;
   }
+  __syncthreads();
+  tile_phase<T>(sgs, to, S, g, G, ncb);
   // the last CTA to finish reduces the chunks' first invalid triplets
   __syncthreads();
   if (tid == 0) {

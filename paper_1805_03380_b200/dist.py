@@ -160,30 +160,62 @@ def spmm_block(k: int, group=None):
     return int(bounds[rank]), int(bounds[rank + 1]), bounds
 
 
-def spmm_exchange(block, bounds, n_rows: int, group=None) -> torch.Tensor:
-    """all_gather of the column blocks (padded to the widest) -> full C."""
-    _, world = _rank_world(group)
+def spmm_exchange(block, bounds, n_rows: int, group=None, dst: Optional[int] = None):
+    """Reassemble C from the column blocks.  C is column-major, so rank q's
+    block C[:, k0:k1] is one contiguous (k1 - k0) * n_rows run of C's storage:
+    * dst=None: every rank gets C -- equal blocks land in C's storage with one
+      all_gather_into_tensor (no padding, no copy after); unequal blocks are
+      padded to the widest block, gathered, and the pad columns dropped;
+    * dst=r: grouped point-to-point sends of the native blocks straight into
+      C's column slices on rank r (exact sizes, no padding); other ranks get
+      None.
+    The result is an (n_rows, k) column-major tensor on the collective device."""
+    rank, world = _rank_world(group)
     tb = _tensor(block, comm_device(group))
     if world == 1:
         return tb
-    width = int(max(bounds[1:] - bounds[:-1]))
-    pad = torch.zeros((n_rows, width), dtype=tb.dtype, device=tb.device)
-    pad[:, : tb.shape[1]] = tb
-    parts = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(parts, pad.contiguous(), group=group)
-    return torch.cat([parts[r][:, : int(bounds[r + 1] - bounds[r])] for r in range(world)], dim=1)
+    widths = [int(bounds[q + 1] - bounds[q]) for q in range(world)]
+    k = int(bounds[-1])
+    flat = tb.t().contiguous().view(-1)  # (k1 - k0) x n_rows: column-major block storage
+    if dst is not None:
+        out = torch.empty((k, n_rows), dtype=tb.dtype, device=tb.device) if rank == dst else None
+        ops = []
+        if rank == dst:
+            for q in range(world):
+                view = out[int(bounds[q]):int(bounds[q + 1])].view(-1)
+                if q == dst:
+                    view.copy_(flat)
+                elif widths[q]:
+                    ops.append(dist.P2POp(dist.irecv, view, q, group))
+        elif widths[rank]:
+            ops.append(dist.P2POp(dist.isend, flat, dst, group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        return out.t() if out is not None else None
+    if len(set(widths)) == 1:
+        out = torch.empty((k, n_rows), dtype=tb.dtype, device=tb.device)
+        dist.all_gather_into_tensor(out.view(-1), flat, group=group)
+        return out.t()
+    width = max(widths)
+    pad = torch.zeros((width, n_rows), dtype=tb.dtype, device=tb.device)
+    pad[: widths[rank]] = flat.view(widths[rank], n_rows)
+    gathered = torch.empty((world, width, n_rows), dtype=tb.dtype, device=tb.device)
+    dist.all_gather_into_tensor(gathered.view(-1), pad.view(-1), group=group)
+    return torch.cat([gathered[q, : widths[q]] for q in range(world)], dim=0).t()
 
 
 def dist_spmm(n_rows: int, n_cols: int, csr, X, group=None, gather: bool = True,
-              local: Optional[Callable] = None):
+              local: Optional[Callable] = None, dst: Optional[int] = None):
     """Each rank computes C[:, k0:k1] for its block of dense columns.
-    Returns the full C (gather=True) or (k0, k1, C_block)."""
+    Returns the full C (gather=True; on rank dst only when dst is given) or
+    (k0, k1, C_block)."""
     local = local or _gpu_spmm_local
     k0, k1, bounds = spmm_block(int(X.shape[1]), group)
     block = local(n_rows, n_cols, csr, X[:, k0:k1])
     if not gather:
         return k0, k1, block
-    return spmm_exchange(block, bounds, n_rows, group)
+    return spmm_exchange(block, bounds, n_rows, group, dst=dst)
 
 
 # ---------------------------------------------------------------------------
@@ -213,52 +245,93 @@ def spgemm_shard(a, b, group=None):
     return c0, c1, bounds, csc_column_slice(*b, c0, c1)
 
 
-def spgemm_exchange(p, r, v, bounds, group=None):
-    """Gather every rank's CSC slice on the collective device: slice sizes,
-    then padded row / value / col_ptr slices; col_ptr rebased by an exclusive
-    scan of the slice nnz.  Returns (col_ptr int64, rows int64, vals f64)."""
-    _, world = _rank_world(group)
+class DistCsc:
+    """A CSC matrix left distributed by column ranges: this rank holds columns
+    [c0, c1) as a standalone CSC slice (col_ptr local), plus every slice's nnz
+    and this slice's global element offset as DEVICE tensors (no host read).
+    `global_col_ptr()` rebases the local col_ptr on the device."""
+
+    def __init__(self, c0, c1, bounds, col_ptr, row_idx, vals, slice_nnz, offset):
+        self.c0, self.c1, self.bounds = c0, c1, bounds
+        self.col_ptr, self.row_idx, self.vals = col_ptr, row_idx, vals
+        self.slice_nnz = slice_nnz  # int64 [world], device
+        self.offset = offset        # int64 [1], device: elements before this slice
+
+    def global_col_ptr(self):
+        return self.col_ptr.to(torch.int64) + self.offset
+
+
+def spgemm_exchange(p, r, v, bounds, group=None, dst: Optional[int] = 0, c_range=None):
+    """Reassemble C = A B from the column slices, native types (int32 indices,
+    float64 values):
+    * one all_gather of the slice nnz (one int64 per rank, device-resident);
+    * dst=None: leave C distributed -- returns a DistCsc whose global offset
+      is an exclusive scan of the gathered nnz on the device (no host read,
+      no bulk transfer);
+    * dst=r: rank r receives every slice by grouped point-to-point transfers
+      (batch_isend_irecv: NCCL grouped send/recv under NCCL) straight into
+      the assembled CSC, col_ptr rebased on the device; returns (col_ptr,
+      rows, vals) on rank r and None elsewhere.  Rank r reads the slice sizes
+      once to size its buffers (the only host synchronisation)."""
+    rank, world = _rank_world(group)
     devc = comm_device(group)
-    p = _tensor(p, devc).to(torch.int64)
-    r = _tensor(r, devc).to(torch.int64)
-    v = _tensor(v, devc).to(torch.float64)
+    p, r, v = _tensor(p, devc), _tensor(r, devc), _tensor(v, devc)
+    nnz = torch.full((1,), r.shape[0], dtype=torch.int64, device=devc)
     if world == 1:
-        return p, r, v
-    nnz = torch.tensor([r.shape[0]], dtype=torch.int64, device=devc)
-    sizes_t = [torch.zeros(1, dtype=torch.int64, device=devc) for _ in range(world)]
-    dist.all_gather(sizes_t, nnz, group=group)
-    sizes = [int(s.item()) for s in sizes_t]
-    cap = max(1, max(sizes))
-    rows_pad = torch.zeros(cap, dtype=torch.int64, device=devc)
-    vals_pad = torch.zeros(cap, dtype=torch.float64, device=devc)
-    rows_pad[: r.shape[0]] = r
-    vals_pad[: v.shape[0]] = v
-    all_rows = [torch.empty_like(rows_pad) for _ in range(world)]
-    all_vals = [torch.empty_like(vals_pad) for _ in range(world)]
-    dist.all_gather(all_rows, rows_pad, group=group)
-    dist.all_gather(all_vals, vals_pad, group=group)
-    wmax = int(max(bounds[1:] - bounds[:-1])) + 1
-    ptr_pad = torch.zeros(wmax, dtype=torch.int64, device=devc)
-    ptr_pad[: p.shape[0]] = p
-    all_ptr = [torch.empty_like(ptr_pad) for _ in range(world)]
-    dist.all_gather(all_ptr, ptr_pad, group=group)
-    col_ptr = [torch.zeros(1, dtype=torch.int64, device=devc)]
-    base = 0
+        sizes = nnz
+    else:
+        sizes = torch.empty(world, dtype=torch.int64, device=devc)
+        dist.all_gather_into_tensor(sizes, nnz, group=group)
+    starts = torch.cumsum(sizes, 0) - sizes
+    if dst is None:
+        c0, c1 = c_range if c_range is not None else (int(bounds[rank]), int(bounds[rank + 1]))
+        return DistCsc(c0, c1, bounds, p, r, v, sizes, starts[rank:rank + 1])
+    if rank != dst:
+        ops = [dist.P2POp(dist.isend, x.contiguous(), dst, group) for x in (r, v, p) if x.numel()]
+        for w in dist.batch_isend_irecv(ops) if ops else []:
+            w.wait()
+        return None
+    host_sizes = sizes.tolist()
+    total = int(sum(host_sizes))
+    n_cols = int(bounds[-1])
+    rows = torch.empty(total, dtype=r.dtype, device=devc)
+    vals = torch.empty(total, dtype=v.dtype, device=devc)
+    col_ptr = torch.empty(n_cols + 1, dtype=torch.int64, device=devc)
+    ptr_parts = []
+    ops = []
+    off = 0
     for q in range(world):
-        width = int(bounds[q + 1] - bounds[q])
-        col_ptr.append(all_ptr[q][1: width + 1] + base)
-        base += sizes[q]
-    return (torch.cat(col_ptr), torch.cat([all_rows[q][: sizes[q]] for q in range(world)]),
-            torch.cat([all_vals[q][: sizes[q]] for q in range(world)]))
+        sz, w = host_sizes[q], int(bounds[q + 1] - bounds[q])
+        rv, vv = rows[off:off + sz], vals[off:off + sz]
+        pq = p if q == dst else torch.empty(w + 1, dtype=p.dtype, device=devc)
+        if q == dst:
+            rv.copy_(r)
+            vv.copy_(v)
+        else:
+            ops += [dist.P2POp(dist.irecv, x, q, group) for x in (rv, vv) if x.numel()]
+            ops.append(dist.P2POp(dist.irecv, pq, q, group))
+        ptr_parts.append(pq)
+        off += sz
+    for w_ in dist.batch_isend_irecv(ops) if ops else []:
+        w_.wait()
+    col_ptr[0] = 0
+    for q in range(world):
+        c0, c1 = int(bounds[q]), int(bounds[q + 1])
+        col_ptr[c0 + 1:c1 + 1] = ptr_parts[q][1:].to(torch.int64) + starts[q]
+    return col_ptr, rows, vals
 
 
 def dist_spgemm(n_rows_a: int, n_inner: int, n_cols_b: int, a, b, group=None,
-                local: Optional[Callable] = None, on_device: bool = False):
-    """C = A B with B's columns split into equal-product ranges; returns the
-    full C on every rank: host arrays (col_ptr int64, rows int64, vals f64),
-    or tensors on the collective device with on_device=True."""
+                local: Optional[Callable] = None, on_device: bool = False, dst: Optional[int] = 0):
+    """C = A B with B's columns split into equal-product ranges.  dst=r:
+    rank r gets the full C -- host arrays (col_ptr int64, rows int64, vals
+    f64), or tensors on the collective device with on_device=True -- and the
+    other ranks None; dst=None: every rank gets its DistCsc slice."""
     local = local or _gpu_spgemm_local
     c0, c1, bounds, sb = spgemm_shard(a, b, group)
     p, r, v = local(n_rows_a, n_inner, c1 - c0, a, sb)
-    out = spgemm_exchange(p, r, v, bounds, group)
-    return out if on_device else tuple(x.cpu().numpy() for x in out)
+    out = spgemm_exchange(p, r, v, bounds, group, dst=dst, c_range=(c0, c1))
+    if out is None or isinstance(out, DistCsc) or on_device:
+        return out
+    cp, rr, vv = out
+    return cp.cpu().numpy().astype(np.int64), rr.cpu().numpy().astype(np.int64), vv.cpu().numpy().astype(np.float64)

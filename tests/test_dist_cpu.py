@@ -73,22 +73,31 @@ def _worker(rank, world, port, q):
         # SpGEMM with skewed columns
         Z1 = _rand_csc(rng, 200, 150, 0, zipf=True)
         Z2 = _rand_csc(rng, 150, 180, 0, zipf=True)
-        P = D.dist_spgemm(200, 150, 180, (Z1[2], Z1[1], Z1[0]), (Z2[2], Z2[1], Z2[0]), local=_oracle_spgemm_local)
-        q.put((rank, t, C.numpy(), P))
+        z1, z2 = (Z1[2], Z1[1], Z1[0]), (Z2[2], Z2[1], Z2[0])
+        P = D.dist_spgemm(200, 150, 180, z1, z2, local=_oracle_spgemm_local, dst=world - 1)
+        # left distributed: this rank's slice with its device-side global offset
+        Dc = D.dist_spgemm(200, 150, 180, z1, z2, local=_oracle_spgemm_local, dst=None)
+        dslice = (Dc.c0, Dc.c1, Dc.global_col_ptr().numpy(), np.asarray(Dc.row_idx), np.asarray(Dc.vals))
+        # C gathered on one rank by point-to-point transfers (uneven column blocks)
+        C1 = D.dist_spmm(n_rows, n_cols, (At[2], At[1], At[0]), X, local=_oracle_spmm_local, dst=0)
+        # equal blocks: one all_gather_into_tensor
+        X4 = rng.standard_normal((n_cols, 4 * world))
+        C4 = D.dist_spmm(n_rows, n_cols, (At[2], At[1], At[0]), X4, local=_oracle_spmm_local)
+        q.put((rank, t, C.numpy(), P, dslice, None if C1 is None else C1.numpy(), C4.numpy()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.timeout(300)
-def test_world2_matches_single_process():
-    world = 2
+@pytest.mark.timeout(400)
+@pytest.mark.parametrize("world", [2, 4])
+def test_world_matches_single_process(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=240) for _ in range(world)]
+    res = [q.get(timeout=300) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -102,11 +111,28 @@ def test_world2_matches_single_process():
     Z1 = _rand_csc(rng, 200, 150, 0, zipf=True)
     Z2 = _rand_csc(rng, 150, 180, 0, zipf=True)
     want_P = oracle.spgemm(200, *Z1, *Z2, 180)
-    for rank, t, C, P in res:
+    X4 = rng.standard_normal((n_cols, 4 * world))
+    want_C4 = oracle.spmm(*A, X4, n_rows, n_cols)
+    covered = 0
+    for rank, t, C, P, dslice, C1, C4 in res:
         assert abs(t - want_t) <= 1e-12 * max(1.0, abs(want_t))
         assert np.array_equal(C, want_C)
-        p, r, v = P
-        assert np.array_equal(p, want_P[2]) and np.array_equal(r, want_P[1]) and np.array_equal(v, want_P[0])
+        assert np.array_equal(C4, want_C4)
+        if rank == 0:
+            assert np.array_equal(C1, want_C)
+        else:
+            assert C1 is None
+        if rank == world - 1:
+            p, r, v = P
+            assert np.array_equal(p, want_P[2]) and np.array_equal(r, want_P[1]) and np.array_equal(v, want_P[0])
+        else:
+            assert P is None
+        c0, c1, gp, r, v = dslice
+        assert np.array_equal(gp, want_P[2][c0:c1 + 1])
+        s, e = want_P[2][c0], want_P[2][c1]
+        assert np.array_equal(r, want_P[1][s:e]) and np.array_equal(v, want_P[0][s:e])
+        covered += c1 - c0
+    assert covered == 180
 
 
 def test_split_by_weight_properties():
