@@ -57,6 +57,7 @@ struct Ws {
   // not initialised
   unsigned* H;
   unsigned* cbcol;
+  unsigned* tile_col;
   long long* own_info;
   unsigned* aM;
   unsigned* aN;
@@ -87,6 +88,7 @@ static size_t carve(Carve& c, Ws<T>* w, long long n, long long nb, long long T_)
   w->bad = c.take<unsigned long long>(1);
   w->H = c.take<unsigned>(hs);
   w->cbcol = c.take<unsigned>(nb + 1);
+  w->tile_col = c.take<unsigned>(std::max(1ll, T_) + 1);
   w->own_info = c.take<long long>(2);
   w->aM = c.take<unsigned>(n1);
   w->aN = c.take<unsigned>(n1);
@@ -164,9 +166,24 @@ static int scan_launch(unsigned* x, long long n, unsigned* total, unsigned long 
 
 // The whole pipeline.  Returns AS_OK after launching, -1 when outside the
 // envelope (the caller falls back to the general bucket kernel).
+template <class T>
+static int prepare(CscIn<T>& s, const Ws<T>& w, cudaStream_t st) {
+  s.tile_col = w.tile_col;
+  if (s.n_cols > 0) {
+    ln_tile_col_kernel<<<(unsigned)((s.n_cols + 255) / 256), 256, 0, st>>>(s.ptr, s.n_cols, s.nnz, w.tile_col);
+    AS_LAUNCH_CHECK();
+  }
+  return AS_OK;
+}
+template <class T, class IdxT>
+static int prepare(CooIn<IdxT, T>&, const Ws<T>&, cudaStream_t) {
+  return AS_OK;
+}
+
 template <class T, class In>
-static int run(const In& src, long long n, long long n_out_cols, int mb, int mode, int prune, int* col_ptr,
-               int* row_idx, T* out_vals, long long* info, void* ws, size_t ws_bytes, cudaStream_t st) {
+static int run(In src, long long n, long long n_out_cols, int mb, int mode, int prune, int* col_ptr,
+               int* row_idx, T* out_vals, long long* info, void* ws, size_t ws_bytes, cudaStream_t st,
+               bool transpose_finish = false) {
   if (disabled()) return -1;
   const Plan p = plan(n, n_out_cols, mb);
   if (!p.ok) return -1;
@@ -180,6 +197,7 @@ static int run(const In& src, long long n, long long n_out_cols, int mb, int mod
   AS_CUDA_TRY(cudaMemsetAsync(w.bad, 0xff, sizeof(unsigned long long), st));
   ln_cbcol_kernel<<<(unsigned)((p.nb + 1 + 255) / 256), 256, 0, st>>>(w.cbcol, p.nb, p.cb_mul, n_out_cols);
   AS_LAUNCH_CHECK();
+  if (int rc = prepare(src, w, st)) return rc;
   Args<T> a;
   a.n = n;
   a.T_ = p.T_;
@@ -215,6 +233,22 @@ static int run(const In& src, long long n, long long n_out_cols, int mb, int mod
     if (int rc = scan_launch(w.H, hs, nullptr, w.st_a, w.tickets + 0, st)) return rc;
     if (int rc = scan_launch(w.bcnt, p.nb, w.bcnt + p.nb, w.st_c, w.tickets + 2, st)) return rc;
     if (int rc = scatter_launch<T, In, 2>(a, src, st)) return rc;
+  }
+  if (mode == kLast && !prune && transpose_finish) {  // every element kept, no duplicates: no sort
+    static bool attr[kMaxDevices] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int smem = (int)sizeof(FinishSmem<T>);
+    if (dev >= 0 && dev < kMaxDevices && !attr[dev]) {
+      AS_CUDA_TRY(cudaFuncSetAttribute(ln_transpose_finish_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem));
+      attr[dev] = true;
+    }
+    const int blocks = (int)std::min<long long>(p.nb, 148ll * 3 * 4);
+    ln_transpose_finish_kernel<T><<<blocks, kT, smem, st>>>(p.nb, w.bcnt, w.bK, w.bV, w.cbcol, mb, n_out_cols,
+                                                           col_ptr, row_idx, out_vals, info);
+    AS_LAUNCH_CHECK();
+    return AS_OK;
   }
   SegLN<T> sg{w.bcnt, w.bK, w.bV, w.cbcol, w.tstate};
   sr::TileOut<T> o;
@@ -255,8 +289,9 @@ int coo_to_csc(long long n_rows, long long n_cols, long long n, const IdxT* rows
 template <class T>
 int transpose(long long n_rows, long long n_cols, long long nnz, const int* col_ptr, const int* row_idx,
               const T* vals, int* t_col_ptr, int* t_row_idx, T* t_vals, void* ws, size_t ws_bytes, cudaStream_t st) {
-  return run<T>(CscIn<T>{col_ptr, row_idx, vals, n_cols, nnz}, nnz, n_rows, bits_for(n_cols > 0 ? n_cols - 1 : 0),
-                kLast, 0, t_col_ptr, t_row_idx, t_vals, nullptr, ws, ws_bytes, st);
+  static const bool generic = getenv("AS_LN_GENERIC_TRANSPOSE") != nullptr;  // A/B: tile-phase finish
+  return run<T>(CscIn<T>{col_ptr, row_idx, vals, n_cols, nnz, nullptr}, nnz, n_rows, bits_for(n_cols > 0 ? n_cols - 1 : 0),
+                kLast, 0, t_col_ptr, t_row_idx, t_vals, nullptr, ws, ws_bytes, st, !generic);
 }
 
 template int coo_to_csc<double, int>(long long, long long, long long, const int*, const int*, const double*, int, int*,

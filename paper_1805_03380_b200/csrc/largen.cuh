@@ -33,13 +33,13 @@
 namespace as {
 namespace ln {
 
-constexpr int kT = 512;          // threads of the count / scatter CTAs
+constexpr int kT = 256;          // threads of the count / scatter / finish CTAs
 constexpr int kI = 8;            // elements per thread
 constexpr int kE = kT * kI;      // elements per pipeline tile
 constexpr int kR = 256;          // digit radix
 constexpr int kW = kT / 32;      // warps
 constexpr int kScanN = 4096;     // entries per scan tile (256 threads x 16)
-constexpr int kJoinSpan = 16;    // low digits a pass-B tile may span for its bucket histogram
+constexpr int kJoinSpan = 2;     // low digits a pass-B tile may span for its bucket histogram (more: global atomics)
 
 // element sources: major (output column), minor (output row), value
 template <class IdxT, class T>
@@ -56,7 +56,18 @@ struct CscIn {  // the elements of a CSC visited by row: major = row, minor = co
   const int* idx;
   const T* vals;
   long long n_cols, nnz;
+  const unsigned* tile_col;  // [T + 1] column of each tile's first element (ln_tile_col_kernel)
 };
+
+// tile_col[t] = the column holding element t * kE (the last column with
+// ptr[c] <= t * kE): every column writes the tiles whose first element it holds
+static __global__ void ln_tile_col_kernel(const int* __restrict__ ptr, long long n_cols, long long nnz,
+                                          unsigned* __restrict__ tile_col) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_cols) return;
+  const long long b = __ldg(&ptr[c]), e = __ldg(&ptr[c + 1]);
+  for (long long t = (b + kE - 1) / kE; t * kE < e; t++) tile_col[t] = (unsigned)c;
+}
 
 template <class T>
 struct RecIn {  // pass A records
@@ -89,73 +100,145 @@ AS_DEVICE_INLINE unsigned bucket_of(unsigned maj, unsigned long long cb_mul) {
   return (unsigned)(((unsigned long long)maj * cb_mul) >> 32);
 }
 
-// ---- element loads of one item: e = global element index; returns valid
-template <class IdxT, class T>
-AS_DEVICE_INLINE bool load_el(const CooIn<IdxT, T>& s, long long e, unsigned& maj, unsigned& mn, T& v,
-                              unsigned long long* bad, bool need_minor, bool need_val) {
-  const long long r = (long long)__ldcs(&s.rows[e]), c = (long long)__ldcs(&s.cols[e]);
-  if (r < 0 || r >= s.n_rows || c < 0 || c >= s.n_cols) {
-    if (bad) atomicMin(bad, (unsigned long long)e);
-    return false;
-  }
-  maj = (unsigned)c;
-  mn = (unsigned)r;
-  if (need_val) v = __ldcs(&s.vals[e]);
-  (void)need_minor;
-  return true;
+// column of maj inside its bucket: maj - cbcol[bucket_of(maj)] = floor(f / cb_mul)
+// with f = maj * cb_mul mod 2^32 (moving d columns down stays in the bucket
+// while d * cb_mul <= f); one 32-bit division, no table lookup
+AS_DEVICE_INLINE unsigned local_col(unsigned maj, unsigned long long cb_mul) {
+  if (cb_mul >> 32) return 0u;  // one column per bucket
+  const unsigned f = (unsigned)((unsigned long long)maj * cb_mul);
+  return f / (unsigned)cb_mul;
 }
 
-// CSC visited by row: the column of element e from the tile's cached column
-// pointers (colc[0..nc] = ptr[cb..cb+nc]) or a global binary search
+// ---- items: every element of a thread is loaded first (all loads in
+// flight together), then decoded.  Item k of a thread is element
+// t * kE + warp * 32 kI + 32 k + lane: warp-blocked and lane-consecutive, so
+// (warp, item, lane) order is the input order and every load is coalesced.
+AS_DEVICE_INLINE long long elem_of(long long t, int k) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  return t * kE + (long long)warp * (32 * kI) + k * 32 + lane;
+}
+
+// upper_bound(ptr[0..N), x) by the whole block (any block size): one sample
+// per thread per round, __syncthreads_count of the samples <= x
+__device__ inline long long blk_upper_bound(const int* ptr, long long N, long long x) {
+  const long long nt = blockDim.x;
+  long long base = 0, len = N;
+  while (len > nt) {
+    const long long step = (len + nt - 1) / nt;
+    const long long j = (long long)threadIdx.x * step;
+    const int c = __syncthreads_count(j < len && __ldg(&ptr[base + j]) <= x);
+    if (c == 0) return base;
+    base += (long long)(c - 1) * step + 1;
+    len = min(step - 1, N - base);
+    if (len <= 0) return base;
+  }
+  const int c = __syncthreads_count((long long)threadIdx.x < len && __ldg(&ptr[base + threadIdx.x]) <= x);
+  return base + c;
+}
+
+// CSC visited by row: the tile's column pointers cached in shared memory
+// (colc[0..nc] = ptr[cb..cb+nc]) when they fit, else global searches
 struct ColCache {
   long long cb;
-  int nc;          // cached entries - 1, or -1 when not cached
+  int nc;  // cached entries - 1, or -1 when not cached
+};
+
+template <class T, class In>
+struct Items;
+
+template <class T, class IdxT>
+struct Items<T, CooIn<IdxT, T>> {
+  IdxT r[kI], c[kI];
+  T v[kI];
+  __device__ void prep(const CooIn<IdxT, T>&, long long, long long, int*, ColCache*) {}
+  template <bool kVal>
+  AS_DEVICE_INLINE void fetch(const CooIn<IdxT, T>& s, int k, long long e) {
+    r[k] = __ldcs(&s.rows[e]);
+    c[k] = __ldcs(&s.cols[e]);
+    if (kVal) v[k] = __ldcs(&s.vals[e]);
+  }
+  // false: an out-of-range triplet (skipped; its index goes to *bad)
+  AS_DEVICE_INLINE bool major(const CooIn<IdxT, T>& s, int k, long long e, unsigned& maj, unsigned long long* bad) {
+    const long long rr = (long long)r[k], cc = (long long)c[k];
+    if (rr < 0 || rr >= s.n_rows || cc < 0 || cc >= s.n_cols) {
+      if (bad) atomicMin(bad, (unsigned long long)e);
+      return false;
+    }
+    maj = (unsigned)cc;
+    return true;
+  }
+  AS_DEVICE_INLINE unsigned minor(const CooIn<IdxT, T>&, int k, long long, const ColCache&, const int*) {
+    return (unsigned)r[k];
+  }
 };
 
 template <class T>
-AS_DEVICE_INLINE bool load_el_csc(const CscIn<T>& s, long long e, const ColCache& cc, const int* colc, unsigned& maj,
-                                  unsigned& mn, T& v, bool need_minor, bool need_val) {
-  maj = (unsigned)__ldcs(&s.idx[e]);
-  if (need_minor) {
-    long long c;
-    if (cc.nc >= 0) {
-      int l = 0, h = cc.nc;  // last l with colc[l] <= e
-      while (l < h) {
-        const int mid = (l + h + 1) >> 1;
-        if (colc[mid] <= e) l = mid;
-        else h = mid - 1;
-      }
-      c = cc.cb + l;
-    } else {
-      c = upper_bound_dev(s.ptr, s.n_cols + 1, (int)e) - 1;
-    }
-    mn = (unsigned)c;
+struct Items<T, CscIn<T>> {
+  int i[kI];
+  T v[kI];
+  long long cur = -1;  // column of this thread's previous element (its elements come in increasing order)
+  __device__ void prep(const CscIn<T>& s, long long lo, long long hi, int* colc, ColCache* cc) {
+    // the columns holding the tile's first / last element (tile_col: one
+    // search per tile boundary, done once for all tiles by ln_tile_col_kernel)
+    const long long t = lo / kE;
+    const long long cb = __ldg(&s.tile_col[t]);
+    const long long ce = hi < s.nnz ? __ldg(&s.tile_col[t + 1]) : s.n_cols - 1;
+    const bool cached = ce - cb + 1 <= sr::kColCache;
+    if (cached)
+      for (long long c = cb + threadIdx.x; c <= ce + 1 && c <= s.n_cols; c += blockDim.x) colc[c - cb] = __ldg(&s.ptr[c]);
+    if (threadIdx.x == 0) *cc = ColCache{cb, cached ? (int)(ce - cb) : -1};
+    __syncthreads();
   }
-  if (need_val) v = __ldcs(&s.vals[e]);
-  return true;
-}
+  template <bool kVal>
+  AS_DEVICE_INLINE void fetch(const CscIn<T>& s, int k, long long e) {
+    i[k] = __ldcs(&s.idx[e]);
+    if (kVal) v[k] = __ldcs(&s.vals[e]);
+  }
+  AS_DEVICE_INLINE bool major(const CscIn<T>&, int k, long long, unsigned& maj, unsigned long long*) {
+    maj = (unsigned)i[k];
+    return true;
+  }
+  AS_DEVICE_INLINE unsigned minor(const CscIn<T>& s, int, long long e, const ColCache& cc, const int* colc) {
+    if (cur < 0) {  // first element: binary search
+      if (cc.nc >= 0) {
+        int l = 0, h = cc.nc;  // last l with colc[l] <= e
+        while (l < h) {
+          const int mid = (l + h + 1) >> 1;
+          if (colc[mid] <= e) l = mid;
+          else h = mid - 1;
+        }
+        cur = cc.cb + l;
+      } else {
+        cur = upper_bound_dev(s.ptr, s.n_cols + 1, (int)e) - 1;
+      }
+    } else if (cc.nc >= 0) {  // advance (32 elements on: a few columns at most)
+      while (colc[cur + 1 - cc.cb] <= e) cur++;
+    } else {
+      while (__ldg(&s.ptr[cur + 1]) <= e) cur++;
+    }
+    return (unsigned)cur;
+  }
+};
 
 template <class T>
-AS_DEVICE_INLINE bool load_el_rec(const RecIn<T>& s, long long e, unsigned& maj, unsigned& mn, T& v, bool need_minor,
-                                  bool need_val) {
-  maj = __ldcs(&s.maj[e]);
-  if (need_minor) mn = __ldcs(&s.mn[e]);
-  if (need_val) v = __ldcs(&s.vals[e]);
-  return true;
-}
-
-// the tile's column range of a CSC source, cached in shared memory when it fits
-template <class T>
-__device__ void csc_cache(const CscIn<T>& s, long long lo, long long hi, int* colc, ColCache* cc) {
-  const long long cb = sr::block_upper_bound(s.ptr, s.n_cols + 1, lo) - 1;
-  const long long ce = sr::block_upper_bound(s.ptr, s.n_cols + 1, hi - 1) - 1;
-  const bool cached = ce - cb + 1 <= sr::kColCache;
-  if (cached)
-    for (long long c = cb + threadIdx.x; c <= ce + 1 && c <= s.n_cols; c += blockDim.x) colc[c - cb] = __ldg(&s.ptr[c]);
-  cc->cb = cb;
-  cc->nc = cached ? (int)(ce - cb) : -1;
-  __syncthreads();
-}
+struct Items<T, RecIn<T>> {
+  unsigned m[kI], n[kI];
+  T v[kI];
+  __device__ void prep(const RecIn<T>&, long long, long long, int*, ColCache*) {}
+  template <bool kVal>
+  AS_DEVICE_INLINE void fetch(const RecIn<T>& s, int k, long long e) {
+    m[k] = __ldcs(&s.maj[e]);
+    if (kVal) {
+      n[k] = __ldcs(&s.mn[e]);
+      v[k] = __ldcs(&s.vals[e]);
+    }
+  }
+  AS_DEVICE_INLINE bool major(const RecIn<T>&, int k, long long, unsigned& maj, unsigned long long*) {
+    maj = m[k];
+    return true;
+  }
+  AS_DEVICE_INLINE unsigned minor(const RecIn<T>&, int k, long long, const ColCache&, const int*) { return n[k]; }
+};
 
 // kind of a pass: 0 = pass A (digit = low bits, writes records A),
 // 1 = pass B from records A (digit = high bits), 2 = single pass (digit = bucket)
@@ -166,83 +249,38 @@ AS_DEVICE_INLINE unsigned digit_of(unsigned b, int lob) {
   return b;
 }
 
-// generic item loader for the three sources
-template <class T, class In>
-struct Loader;
-
-template <class T, class IdxT>
-struct Loader<T, CooIn<IdxT, T>> {
-  const CooIn<IdxT, T>& s;
-  unsigned long long* bad;
-  __device__ void prep(long long, long long, int*, ColCache*) {}
-  AS_DEVICE_INLINE bool operator()(long long e, unsigned& maj, unsigned& mn, T& v, bool need_minor, bool need_val,
-                                   const ColCache&, const int*) {
-    return load_el(s, e, maj, mn, v, bad, need_minor, need_val);
-  }
-};
-
-template <class T>
-struct Loader<T, CscIn<T>> {
-  const CscIn<T>& s;
-  unsigned long long* bad;
-  __device__ void prep(long long lo, long long hi, int* colc, ColCache* cc) { csc_cache(s, lo, hi, colc, cc); }
-  AS_DEVICE_INLINE bool operator()(long long e, unsigned& maj, unsigned& mn, T& v, bool need_minor, bool need_val,
-                                   const ColCache& cc, const int* colc) {
-    return load_el_csc(s, e, cc, colc, maj, mn, v, need_minor, need_val);
-  }
-};
-
-template <class T>
-struct Loader<T, RecIn<T>> {
-  const RecIn<T>& s;
-  unsigned long long* bad;
-  __device__ void prep(long long, long long, int*, ColCache*) {}
-  AS_DEVICE_INLINE bool operator()(long long e, unsigned& maj, unsigned& mn, T& v, bool need_minor, bool need_val,
-                                   const ColCache&, const int*) {
-    return load_el_rec(s, e, maj, mn, v, need_minor, need_val);
-  }
-};
-
-// element e of item k of this thread: warp-blocked, lane-consecutive, so the
-// (warp, item, lane) order is the input order
-AS_DEVICE_INLINE long long elem_of(long long t, int k) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  return t * kE + (long long)warp * (32 * kI) + k * 32 + lane;
-}
-
 // ------------------------------------------------------------------------
 // count: digit histogram of tile t -> H[d * T + t]; pass 1 / 2 also add the
 // tile's bucket counts into bcnt
 template <class T, class In, int kPass>
 __global__ void __launch_bounds__(kT) ln_count_kernel(Args<T> a, In src) {
   __shared__ unsigned h[kR];
-  __shared__ unsigned jb[kJoinSpan * kR];
-  __shared__ int colc[sr::kColCache + 1];
-  __shared__ ColCache cc;
+  __shared__ unsigned jb[kPass == 1 ? kJoinSpan * kR : 1];
   __shared__ unsigned lo0s;
   const int tid = threadIdx.x;
   const long long t = blockIdx.x;
   const long long lo = t * kE, hi = min(a.n, lo + kE);
   for (int i = tid; i < kR; i += kT) h[i] = 0u;
-  if (kPass == 1)
-    for (int i = tid; i < kJoinSpan * kR; i += kT) jb[i] = 0u;
-  Loader<T, In> ld{src, kPass != 1 ? a.bad : nullptr};
-  if (tid == 0) cc = ColCache{0, -1};
   if constexpr (kPass == 1) {
+    for (int i = tid; i < kJoinSpan * kR; i += kT) jb[i] = 0u;
     if (tid == 0) lo0s = bucket_of(__ldg(&src.maj[lo]), a.cb_mul) & ((1u << a.lob) - 1u);
+  }
+  Items<T, In> it;
+#pragma unroll
+  for (int k = 0; k < kI; k++) {
+    const long long e = elem_of(t, k);
+    if (e < hi) it.template fetch<false>(src, k, e);
   }
   __syncthreads();
   const unsigned lo0 = kPass == 1 ? lo0s : 0u;
 #pragma unroll
   for (int k = 0; k < kI; k++) {
     const long long e = elem_of(t, k);
-    if (e >= hi) continue;
-    unsigned maj = 0, mn = 0;
-    T v;
-    if (!ld(e, maj, mn, v, false, false, cc, colc)) continue;
+    unsigned maj;
+    if (e >= hi || !it.major(src, k, e, maj, kPass != 1 ? a.bad : nullptr)) continue;
     const unsigned b = bucket_of(maj, a.cb_mul);
     atomicAdd(&h[digit_of<kPass>(b, a.lob)], 1u);
-    if (kPass == 1) {
+    if constexpr (kPass == 1) {
       const unsigned lw = (b & ((1u << a.lob) - 1u)) - lo0;
       if (lw < (unsigned)kJoinSpan) atomicAdd(&jb[lw * kR + (b >> a.lob)], 1u);
       else atomicAdd(&a.bcnt[b], 1u);
@@ -254,7 +292,7 @@ __global__ void __launch_bounds__(kT) ln_count_kernel(Args<T> a, In src) {
     a.H[(long long)d * a.T_ + t] = h[d];
     if (kPass == 2 && h[d]) atomicAdd(&a.bcnt[d], h[d]);
   }
-  if (kPass == 1) {
+  if constexpr (kPass == 1) {
     for (int i = tid; i < kJoinSpan * kR; i += kT) {
       if (jb[i]) {
         const unsigned b = ((unsigned)(i % kR) << a.lob) | (lo0 + (unsigned)(i / kR));
@@ -311,51 +349,61 @@ struct ScatterSmem {
   unsigned tstart[kR];      // tile-local digit starts
   unsigned gbase[kR];       // global start of the tile's run of each digit
   unsigned k1[kE];          // major (pass A) or bucket-local key
-  unsigned k2[kE];          // minor (pass A only)
+  unsigned k2[kPass == 0 ? kE : 1];  // minor (pass A only)
   T v[kE];
-  unsigned short d[kE];
+  unsigned char d[kE];
   long long scan[kT / 32 + 1];
   int colc[sr::kColCache + 1];
   ColCache cc;
 };
 
+#ifndef AS_LN_SCATTER_MINB
+#define AS_LN_SCATTER_MINB 4
+#endif
 template <class T, class In, int kPass>
-__global__ void __launch_bounds__(kT, 2) ln_scatter_kernel(Args<T> a, In src) {
+__global__ void __launch_bounds__(kT, AS_LN_SCATTER_MINB) ln_scatter_kernel(Args<T> a, In src) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ScatterSmem<T, kPass>& S = *reinterpret_cast<ScatterSmem<T, kPass>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long t = blockIdx.x;
   const long long lo = t * kE, hi = min(a.n, lo + kE);
-  Loader<T, In> ld{src, nullptr};
-  if (tid == 0) S.cc = ColCache{0, -1};
+  const int R = kPass == 0 ? (1 << a.lob) : kR;
+  const unsigned gb = tid < R ? __ldcg(&a.H[(long long)tid * a.T_ + t]) : 0u;  // the tile's run offsets, early
+  Items<T, In> it;
+#pragma unroll
+  for (int k = 0; k < kI; k++) {  // every load of the tile in flight first
+    const long long e = elem_of(t, k);
+    if (e < hi) it.template fetch<true>(src, k, e);
+  }
   for (int i = lane; i < kR; i += 32) S.wc[warp][i] = 0u;
+  it.prep(src, lo, hi, S.colc, &S.cc);  // (CSC source: the tile's column pointers; syncs)
   __syncthreads();
-  ld.prep(lo, hi, S.colc, &S.cc);  // (CSC source: block-wide; others no-op)
   const ColCache cc = S.cc;
-  unsigned maj[kI], mn[kI], dg[kI], rk[kI];
-  T v[kI];
-  bool ok[kI];
+  unsigned dg[kI], rk[kI];
 #pragma unroll
   for (int k = 0; k < kI; k++) {
     const long long e = elem_of(t, k);
-    ok[k] = e < hi && ld(e, maj[k], mn[k], v[k], true, true, cc, S.colc);
-    dg[k] = ok[k] ? digit_of<kPass>(bucket_of(maj[k], a.cb_mul), a.lob) : 0xffffu;
+    unsigned maj = 0;
+    const bool ok = e < hi && it.major(src, k, e, maj, nullptr);
+    dg[k] = ok ? digit_of<kPass>(bucket_of(maj, a.cb_mul), a.lob) : 0xffffu;
   }
-  // stable ranks: item by item (input order), lanes of one digit by match
+  // stable ranks: item by item (input order); the lanes of one digit by match
 #pragma unroll
   for (int k = 0; k < kI; k++) {
     const unsigned peers = __match_any_sync(0xffffffffu, dg[k]);
+    const bool ok = dg[k] != 0xffffu;
     unsigned base = 0;
-    if (ok[k]) base = S.wc[warp][dg[k]];
+    if (ok) base = S.wc[warp][dg[k]];
     rk[k] = base + __popc(peers & lanemask_lt());
     __syncwarp();
-    if (ok[k] && (peers & lanemask_lt()) == 0u) S.wc[warp][dg[k]] = base + __popc(peers);
+    if (ok && (peers & lanemask_lt()) == 0u) S.wc[warp][dg[k]] = base + __popc(peers);
     __syncwarp();
   }
   __syncthreads();
   // per digit: offsets of the warps (in warp order), tile count, tile start
   unsigned cnt = 0;
   if (tid < kR) {
+#pragma unroll
     for (int w = 0; w < kW; w++) {
       const unsigned c = S.wc[w][tid];
       S.wc[w][tid] = cnt;
@@ -364,25 +412,27 @@ __global__ void __launch_bounds__(kT, 2) ln_scatter_kernel(Args<T> a, In src) {
   }
   long long tot;
   const long long st = block_exclusive_scan<long long>(tid < kR ? (long long)cnt : 0ll, S.scan, &tot);
-  const int R = kPass == 0 ? (1 << a.lob) : kR;
   if (tid < kR) {
     S.tstart[tid] = (unsigned)st;
-    S.gbase[tid] = tid < R ? __ldcg(&a.H[(long long)tid * a.T_ + t]) : 0u;
+    S.gbase[tid] = gb;
   }
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < kI; k++) {
-    if (!ok[k]) continue;
+    if (dg[k] == 0xffffu) continue;
+    const long long e = elem_of(t, k);
     const unsigned p = S.tstart[dg[k]] + S.wc[warp][dg[k]] + rk[k];
+    unsigned maj = 0;
+    it.major(src, k, e, maj, nullptr);
+    const unsigned mn = it.minor(src, k, e, cc, S.colc);
     if (kPass == 0) {
-      S.k1[p] = maj[k];
-      S.k2[p] = mn[k];
+      S.k1[p] = maj;
+      S.k2[p] = mn;
     } else {
-      const unsigned b = bucket_of(maj[k], a.cb_mul);
-      S.k1[p] = ((maj[k] - __ldg(&a.cbcol[b])) << a.mb) | mn[k];
+      S.k1[p] = (local_col(maj, a.cb_mul) << a.mb) | mn;
     }
-    S.v[p] = v[k];
-    S.d[p] = (unsigned short)dg[k];
+    S.v[p] = it.v[k];
+    S.d[p] = (unsigned char)dg[k];
   }
   __syncthreads();
   const unsigned m = (unsigned)tot;
@@ -443,6 +493,152 @@ ln_tiles_kernel(SegLN<T> sg_, sr::TileOut<T> o_, long long nb, const unsigned lo
     o.info[1] = b < (unsigned long long)n ? (long long)b : 0x7f7f7f7f7f7f7f7fll;
   }
   sr::tile_phase<T>(sg, o, S, blockIdx.x, gridDim.x, nb);
+}
+
+// Transpose finish, one CTA per bucket (no look-back): a transpose keeps
+// every element, so bucket t's output is exactly the slots [bstart[t],
+// bstart[t+1]); its rows' pointers are bstart[t] + a scan of the bucket's
+// per-row counts, and each element's place in its row is its stable rank --
+// the bucket's slots are in input (column-major) order, so the rank by arrival
+// IS the column order the output needs.  No sort, no reduce, any bucket size
+// (chunks of kE elements in order, running row cursors); a bucket that fits
+// one chunk is staged in shared memory and written out coalesced.
+template <class T>
+struct FinishSmem {
+  unsigned wc[kW][sr::kMaxW];  // per-warp row counters -> offsets within the chunk
+  unsigned run[sr::kMaxW];     // row cursors (bucket-local output position)
+  unsigned ctot[sr::kMaxW];    // the chunk's count of each row
+  unsigned rk[kE];             // staged output rows
+  T v[kE];                     // staged output values
+  unsigned long long scan[kT / 32 + 1];
+};
+
+template <class T>
+__global__ void __launch_bounds__(kT, 3)
+ln_transpose_finish_kernel(long long nb, const unsigned* __restrict__ bstart, const unsigned* __restrict__ bK,
+                           const T* __restrict__ bV, const unsigned* __restrict__ cbcol, int mb, long long n_out_cols,
+                           int* __restrict__ col_ptr, int* __restrict__ row_idx, T* __restrict__ out_vals,
+                           long long* info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FinishSmem<T>& S = *reinterpret_cast<FinishSmem<T>*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned mmask = mb >= 32 ? 0xffffffffu : ((1u << mb) - 1u);
+  if (blockIdx.x == 0 && tid == 0) {
+    const unsigned n = __ldg(&bstart[nb]);
+    col_ptr[n_out_cols] = (int)n;
+    if (info) info[0] = n;
+  }
+  for (long long t = blockIdx.x; t < nb; t += gridDim.x) {
+    const unsigned s0 = __ldg(&bstart[t]), L = __ldg(&bstart[t + 1]) - s0;
+    const unsigned c0 = __ldg(&cbcol[t]);
+    const int W = (int)(__ldg(&cbcol[t + 1]) - c0);
+    const bool one = L <= (unsigned)kE;
+    // the first chunk's loads go out before anything waits
+    unsigned key[kI];
+    T v[kI];
+#pragma unroll
+    for (int k = 0; k < kI; k++) {
+      const unsigned i = warp * (32 * kI) + k * 32 + lane;
+      if (i < L) {
+        key[k] = __ldcs(&bK[s0 + i]);
+        v[k] = __ldcs(&bV[s0 + i]);
+      }
+    }
+    __syncthreads();  // the previous bucket's shared memory is free
+    for (int l = tid; l < W; l += kT) S.run[l] = 0u;
+    __syncthreads();
+    // row counts of the whole bucket -> row starts (run) and col_ptr
+    if (one) {
+#pragma unroll
+      for (int k = 0; k < kI; k++)
+        if (warp * (32 * kI) + k * 32 + lane < L) atomicAdd(&S.run[key[k] >> mb], 1u);
+    } else {
+      for (unsigned i = tid; i < L; i += kT) atomicAdd(&S.run[__ldcs(&bK[s0 + i]) >> mb], 1u);
+    }
+    __syncthreads();
+    {
+      constexpr int kPerT = (sr::kMaxW + kT - 1) / kT;
+      unsigned c[kPerT], sum = 0;
+#pragma unroll
+      for (int q = 0; q < kPerT; q++) {
+        const int l = tid * kPerT + q;
+        c[q] = l < W ? S.run[l] : 0u;
+        sum += c[q];
+      }
+      unsigned long long tot;
+      unsigned long long ex = block_exclusive_scan<unsigned long long>(sum, S.scan, &tot);
+#pragma unroll
+      for (int q = 0; q < kPerT; q++) {
+        const int l = tid * kPerT + q;
+        if (l < W) {
+          S.run[l] = (unsigned)ex;
+          col_ptr[c0 + l] = (int)(s0 + ex);
+        }
+        ex += c[q];
+      }
+    }
+    for (unsigned base = 0; base < L; base += kE) {  // chunks in input order
+      if (base > 0) {
+#pragma unroll
+        for (int k = 0; k < kI; k++) {
+          const unsigned i = base + warp * (32 * kI) + k * 32 + lane;
+          if (i < L) {
+            key[k] = __ldcs(&bK[s0 + i]);
+            v[k] = __ldcs(&bV[s0 + i]);
+          }
+        }
+      }
+      for (int l = lane; l < W; l += 32) S.wc[warp][l] = 0u;
+      __syncwarp();
+      unsigned rk[kI], lr[kI];
+#pragma unroll
+      for (int k = 0; k < kI; k++) {
+        const bool in = base + warp * (32 * kI) + k * 32 + lane < L;
+        lr[k] = in ? key[k] >> mb : 0xffffffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, lr[k]);
+        unsigned b0 = 0;
+        if (in) b0 = S.wc[warp][lr[k]];
+        rk[k] = b0 + __popc(peers & lanemask_lt());
+        __syncwarp();
+        if (in && (peers & lanemask_lt()) == 0u) S.wc[warp][lr[k]] = b0 + __popc(peers);
+        __syncwarp();
+      }
+      __syncthreads();
+      for (int l = tid; l < W; l += kT) {  // per row: warp offsets (warp order), chunk count
+        unsigned run = 0;
+#pragma unroll
+        for (int w = 0; w < kW; w++) {
+          const unsigned c = S.wc[w][l];
+          S.wc[w][l] = run;
+          run += c;
+        }
+        S.ctot[l] = run;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kI; k++) {
+        if (lr[k] == 0xffffffffu) continue;
+        const unsigned p = S.run[lr[k]] + S.wc[warp][lr[k]] + rk[k];  // bucket-local output position
+        if (one) {
+          S.rk[p] = key[k] & mmask;
+          S.v[p] = v[k];
+        } else {
+          __stcs(&row_idx[s0 + p], (int)(key[k] & mmask));
+          __stcs(&out_vals[s0 + p], v[k]);
+        }
+      }
+      __syncthreads();
+      if (one) {
+        for (unsigned q = tid; q < L; q += kT) {
+          __stcs(&row_idx[s0 + q], (int)S.rk[q]);
+          __stcs(&out_vals[s0 + q], S.v[q]);
+        }
+      } else {
+        for (int l = tid; l < W; l += kT) S.run[l] += S.ctot[l];
+        __syncthreads();
+      }
+    }
+  }
 }
 
 // first column of every bucket: cbcol[b] = ceil(b * 2^32 / cb_mul) (capped)
