@@ -751,6 +751,30 @@ def bench_ops(args, dev, L, sp, timed, peak):
                {"mode": "f32 FMA, CSR cached on the handle", "exact_mode_ms": t_exact,
                 "launches": 2 * ((k + 15) // 16)})
 
+        # the first product on a fresh CSC handle (the reference's
+        # mat_times_vec walks the CSC; here the handle builds its CSR once, with
+        # the large-input transpose, and keeps it): conversion + SpMM, public API
+        from paper_1805_03380_b200 import SpMat
+        from paper_1805_03380_b200.csc import CscData, Dims
+
+        A_csc = CscData(Dims(n, n), p, r, v)
+
+        def f_first():
+            return SpMat.from_csc(A_csc) @ Bd
+
+        f_fast()
+        C_ref = C.clone()
+        C_first = f_first()
+        torch.cuda.synchronize()
+        if not torch.equal(C_first, C_ref):
+            raise CorrectnessError("first-call SpMM differs from the cached-CSR SpMM")
+        del C_first, C_ref
+        t_first = timed(f_first, K, W)
+        tt = statistics.median(timed(lambda: _kernels.transpose(n, n, p, r, v), K, W))
+        record("spmm_cfg3_first_call", t_first, alg / 1e9, "GB/s", alg, "identical to the cached-CSR SpMM",
+               {"path": "SpMat.from_csc(fresh CSC) @ B: CSC->CSR transpose (large-input pipeline) + row-split SpMM",
+                "transpose_ms": tt, "launches": 11 + 2 * ((k + 15) // 16)})
+
     # fused trace (cfg4)
     if "trace" in want_ops:
         n, _, A, Bm = synth.cfg4_trace_pair()
@@ -830,6 +854,32 @@ def bench_ops(args, dev, L, sp, timed, peak):
             record("spgemm_cfg5", timed(f, max(3, K // 4), W), total, "products/s",
                    12 * (na + nb) + 8 * (n + 1) + 12 * nnz + 4 * (n + 1), parity,
                    {"products": total, "nnz_out": nnz, "launches": 6})
+            # the same product through the public API (SpMat @ SpMat -> ops.matmul ->
+            # _kernels.spgemm: sizing read-backs and allocation included), wall clock
+            from paper_1805_03380_b200 import SpMat
+            from paper_1805_03380_b200.csc import CscData, Dims
+
+            SA = SpMat.from_csc(CscData(Dims(n, n), *a))
+            SB = SpMat.from_csc(CscData(Dims(n, n), *b))
+            del cr, cv, ws
+            torch.cuda.empty_cache()
+            api = []
+            for i in range(W + max(3, K // 4)):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                P = SA @ SB
+                Pc = P.csc()
+                torch.cuda.synchronize()
+                if i >= W:
+                    api.append(time.perf_counter() - t0)
+                del P, Pc
+            out["spgemm_cfg5"]["api_ms"] = 1e3 * statistics.median(api)
+            out["spgemm_cfg5"]["api_path"] = "SpMat A @ SpMat B -> CSC on the device (wall clock, host syncs included)"
+
+    # beyond BASELINE sizes: the bandwidth regime the north star's 60 % target
+    # refers to (the large-input pipeline, csrc/largen.cuh)
+    if "large" in want_ops:
+        out["large_n"] = bench_large_n(args, dev, L, sp, timed, peak)
 
     # SURVEY 8f-2 ("next" rows): construction-funnelled ops and segmented
     # reductions through the public ops API on the cfg 1 matrix (10k x 10k,
@@ -923,6 +973,117 @@ def bench_ops(args, dev, L, sp, timed, peak):
     return out
 
 
+def bench_large_n(args, dev, L, sp, timed, peak):
+    """Construction and transpose at 1e7 / 1e8 / 5e7 elements (seeded uniform
+    coordinates, values U[-1,1]), each checked first: bit-exact against the
+    oracle at 1e7, by properties at the larger sizes (strictly increasing
+    (column, row) keys, nnz = distinct input keys, value sum; transpose
+    involution and row histogram)."""
+    import torch
+
+    import oracle
+    from paper_1805_03380_b200._lib import ptr
+    from paper_1805_03380_b200.errors import CorrectnessError
+
+    cases = [("build_1e7", "build", 1_000_000, 1_000_000, 10_000_000, torch.float64),
+             ("build_1e8", "build", 10_000_000, 10_000_000, 100_000_000, torch.float64),
+             ("transpose_1e7_f32", "transpose", 1_000_000, 1_000_000, 10_000_000, torch.float32),
+             ("transpose_5e7", "transpose", 5_000_000, 5_000_000, 50_000_000, torch.float64)]
+    res = {}
+    K, W = max(3, args.op_steps // 2), args.warmup
+    for name, op, n_rows, n_cols, n, vdt in cases:
+        g = torch.Generator(device=dev)
+        g.manual_seed(7)
+        rows = torch.randint(0, n_rows, (n,), device=dev, dtype=torch.int32, generator=g)
+        cols = torch.randint(0, n_cols, (n,), device=dev, dtype=torch.int32, generator=g)
+        vals = (torch.rand(n, device=dev, dtype=torch.float64, generator=g) * 2 - 1).to(vdt)
+        vb = 8 if vdt == torch.float64 else 4
+        cp = torch.empty(n_cols + 1, dtype=torch.int32, device=dev)
+        ri = torch.empty(n, dtype=torch.int32, device=dev)
+        ov = torch.empty(n, dtype=vdt, device=dev)
+        info = torch.empty(2, dtype=torch.int64, device=dev)
+        wb = L.as_build_workspace_bytes(n, n_cols)
+        ws = torch.empty(wb, dtype=torch.uint8, device=dev)
+        fb = L.as_coo_to_csc_f64 if vdt == torch.float64 else L.as_coo_to_csc_f32
+
+        def build():
+            _lib_check(fb(n_rows, n_cols, n, ptr(rows), ptr(cols), 4, ptr(vals), 0, ptr(cp), ptr(ri), ptr(ov),
+                          ptr(info), ptr(ws), wb, sp))
+
+        build()
+        torch.cuda.synchronize()
+        nnz = int(info[0].item())
+        if op == "build":
+            if n <= 20_000_000:
+                want = oracle.canonicalize(n_rows, n_cols, rows.cpu().numpy().astype(np.int64),
+                                           cols.cpu().numpy().astype(np.int64), vals.cpu().numpy().astype(np.float64))
+                ok = (np.array_equal(cp.cpu().numpy(), want[2]) and np.array_equal(ri[:nnz].cpu().numpy(), want[1])
+                      and np.array_equal(ov[:nnz].cpu().numpy(), want[0]))
+                parity = "bit-exact vs oracle"
+            else:
+                cnt = (cp[1:] - cp[:-1]).long()
+                colx = torch.repeat_interleave(torch.arange(n_cols, device=dev), cnt)
+                keys = colx * n_rows + ri[:nnz].long()
+                distinct = int(torch.unique(cols.long() * n_rows + rows.long()).numel())
+                s_in, s_out = float(vals.double().sum()), float(ov[:nnz].double().sum())
+                ok = (bool((keys[1:] > keys[:-1]).all()) and distinct == nnz and int(cp[-1]) == nnz
+                      and abs(s_in - s_out) <= 1e-9 * max(1.0, abs(s_in)))
+                parity = "strictly increasing (col,row) keys, nnz = distinct input keys, value sum within 1e-9"
+                del cnt, colx, keys
+            if not ok:
+                raise CorrectnessError("%s differs from the oracle / properties" % name)
+            alg = (8 + vb) * n + (4 + vb) * nnz + 4 * (n_cols + 1)
+            t = timed(build, K, W)
+            units = n
+        else:
+            p, r, v = cp.clone(), ri[:nnz].clone(), ov[:nnz].clone()
+            del ws
+            tp = torch.empty(n_rows + 1, dtype=torch.int32, device=dev)
+            tr = torch.empty(nnz, dtype=torch.int32, device=dev)
+            tv = torch.empty(nnz, dtype=vdt, device=dev)
+            ft = L.as_csc_transpose_f64 if vdt == torch.float64 else L.as_csc_transpose_f32
+            wbt = L.as_transpose_workspace_bytes(nnz, n_rows)
+            wst = torch.empty(wbt, dtype=torch.uint8, device=dev)
+
+            def tr_fn():
+                _lib_check(ft(n_rows, n_cols, nnz, ptr(p), ptr(r), ptr(v), ptr(tp), ptr(tr), ptr(tv), ptr(wst), wbt,
+                              sp))
+
+            tr_fn()
+            torch.cuda.synchronize()
+            if nnz <= 20_000_000:
+                want = oracle.transpose(n_rows, n_cols, v.cpu().numpy().astype(np.float64),
+                                        r.cpu().numpy().astype(np.int64), p.cpu().numpy().astype(np.int64))
+                ok = (np.array_equal(tp.cpu().numpy(), want[2]) and np.array_equal(tr.cpu().numpy(), want[1])
+                      and np.array_equal(tv.cpu().numpy().astype(np.float64), want[0]))
+                parity = "bit-exact vs oracle"
+            else:
+                bp, br, bv = torch.empty_like(p), torch.empty_like(r), torch.empty_like(v)
+                _lib_check(ft(n_cols, n_rows, nnz, ptr(tp), ptr(tr), ptr(tv), ptr(bp), ptr(br), ptr(bv), ptr(wst), wbt,
+                              sp))
+                ok = (torch.equal(bp, p) and torch.equal(br, r) and torch.equal(bv, v)
+                      and torch.equal((tp[1:] - tp[:-1]).long(), torch.bincount(r.long(), minlength=n_rows)))
+                parity = "involution (A^T)^T == A bit-exact, row histogram"
+                del bp, br, bv
+            if not ok:
+                raise CorrectnessError("%s differs from the oracle / properties" % name)
+            alg = 2 * (4 + vb) * nnz + 4 * (n_cols + 1) + 4 * (n_rows + 1)
+            t = timed(tr_fn, K, W)
+            units = nnz
+            del p, r, v, tp, tr, tv, wst
+        ms = statistics.median(t)
+        gbs = alg / (ms * 1e-3) / 1e9
+        res[name] = {"ms": ms, "value": units / (ms * 1e-3), "unit": "elements/s", "n": n, "nnz_out": nnz,
+                     "shape": [n_rows, n_cols], "dtype": "f64" if vb == 8 else "f32",
+                     "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                                  "algorithmic_bytes": alg, "traffic": ncu_traffic(name),
+                                  "traffic_launches": ncu_launches(name)},
+                     "parity": parity, "engine": "large-input pipeline (csrc/largen.cuh)"}
+        del rows, cols, vals, cp, ri, ov, info
+        torch.cuda.empty_cache()
+    return res
+
+
 def _lib_check(rc):
     from paper_1805_03380_b200 import _lib
 
@@ -935,7 +1096,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--ops", default="transpose,flush,flush_api,spmm,trace,add,spgemm,next")
+    ap.add_argument("--ops", default="transpose,flush,flush_api,spmm,trace,add,spgemm,large,next")
     ap.add_argument("--op-steps", type=int, default=10)
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

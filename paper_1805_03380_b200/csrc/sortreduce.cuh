@@ -49,7 +49,10 @@ constexpr int kPer = 8;                        // P1: elements per thread (two g
 constexpr int kChunkMax = kThreads * kPer;     // elements per CTA chunk
 constexpr int kTile = 2048;                    // elements of a shared-memory tile
 constexpr int kTP = kTile / kThreads;          // tile elements per thread
-constexpr int kNB = 1024;                      // bins per tile
+#ifndef AS_SR_NB
+#define AS_SR_NB 1024
+#endif
+constexpr int kNB = AS_SR_NB;                  // bins per tile
 constexpr int kMaxW = 1024;                    // columns per bucket
 constexpr int kRankMax = 32;                   // bins up to this rank by counting
 constexpr int kColCache = 1024;                // CSC source: cached column pointers of a chunk

@@ -12,13 +12,15 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_1805_03380_b200 import _kernels, synth  # noqa: E402
+from paper_1805_03380_b200 import SpMat, _kernels, synth  # noqa: E402
+from paper_1805_03380_b200.csc import CscData, Dims  # noqa: E402
 
 
 def main():
     op = sys.argv[1]
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-    for o in (("build", "transpose", "flush", "spmm", "trace", "add", "spgemm") if op == "all" else (op,)):
+    for o in (("build", "transpose", "flush", "spmm", "spmm_first", "trace", "add", "spgemm", "build_1e7",
+               "transpose_1e7_f32") if op == "all" else (op,)):
         run(o, reps)
 
 
@@ -62,8 +64,23 @@ def run(op, reps):
             with rng_(op):
                 if op == "spmm":
                     _kernels.spmm(n, n, csr, Bd)
-                else:  # first product on a fresh CSC handle: whatever conversion it needs is part of the op
-                    _kernels.spmm_csc(n, n, a, Bd)
+                else:  # first product on a fresh CSC handle: its CSR conversion is part of the op
+                    SpMat.from_csc(CscData(Dims(n, n), *a)) @ Bd
+    elif op in ("build_1e7", "transpose_1e7_f32"):  # large-input pipeline (bench.py bench_large_n)
+        n = 1_000_000
+        g = torch.Generator(device=dev)
+        g.manual_seed(7)
+        vdt = torch.float64 if op == "build_1e7" else torch.float32
+        rows = torch.randint(0, n, (10_000_000,), device=dev, dtype=torch.int32, generator=g)
+        cols = torch.randint(0, n, (10_000_000,), device=dev, dtype=torch.int32, generator=g)
+        vals = (torch.rand(10_000_000, device=dev, dtype=torch.float64, generator=g) * 2 - 1).to(vdt)
+        p, ri, vv, _ = _kernels.coo_to_csc(n, n, rows, cols, vals)
+        for _ in range(reps):
+            with rng_(op):
+                if op == "build_1e7":
+                    _kernels.coo_to_csc(n, n, rows, cols, vals)
+                else:
+                    _kernels.transpose(n, n, p, ri, vv)
     elif op in ("trace", "add", "spgemm"):
         if op == "trace":
             n, _, A, B = synth.cfg4_trace_pair()
