@@ -235,9 +235,18 @@ static int run(In src, long long n, long long n_out_cols, int mb, int mode, int 
     if (int rc = scatter_launch<T, In, 2>(a, src, st)) return rc;
   }
   if (mode == kLast && !prune && transpose_finish) {  // every element kept, no duplicates: no sort
-    const int blocks = (int)std::min<long long>((p.nb + kFW - 1) / kFW, 148ll * 8);
-    ln_transpose_finish_kernel<T><<<blocks, 32 * kFW, 0, st>>>(p.nb, w.bcnt, w.bK, w.bV, w.cbcol, mb, n_out_cols,
-                                                               col_ptr, row_idx, out_vals, info);
+    static bool attr[kMaxDevices] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int smem = (int)sizeof(FinishSmem<T>);
+    if (dev >= 0 && dev < kMaxDevices && !attr[dev]) {
+      AS_CUDA_TRY(cudaFuncSetAttribute(ln_transpose_finish_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem));
+      attr[dev] = true;
+    }
+    const int blocks = (int)std::min<long long>(p.nb, 148ll * 3 * 4);
+    ln_transpose_finish_kernel<T><<<blocks, kT, smem, st>>>(p.nb, w.bcnt, w.bK, w.bV, w.cbcol, mb, n_out_cols,
+                                                           col_ptr, row_idx, out_vals, info);
     AS_LAUNCH_CHECK();
     return AS_OK;
   }

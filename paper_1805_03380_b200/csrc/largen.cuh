@@ -495,93 +495,149 @@ ln_tiles_kernel(SegLN<T> sg_, sr::TileOut<T> o_, long long nb, const unsigned lo
   sr::tile_phase<T>(sg, o, S, blockIdx.x, gridDim.x, nb);
 }
 
-// Transpose finish, one warp per bucket, no look-back: a transpose keeps
+// Transpose finish, one CTA per bucket (no look-back): a transpose keeps
 // every element, so bucket t's output is exactly the slots [bstart[t],
 // bstart[t+1]); its rows' pointers are bstart[t] + a scan of the bucket's
 // per-row counts, and each element's place in its row is its stable rank --
 // the bucket's slots are in input (column-major) order, so the rank by arrival
-// IS the column order the output needs.  No sort, no reduce, no CTA barrier:
-// the warp walks its bucket twice in batches of 8 elements per lane (all
-// loads of a batch in flight together) -- counts, then placement in order
-// (match_any ranks the lanes of one row; per-row cursors in shared memory).
-constexpr int kFW = 8;  // warps per CTA
+// IS the column order the output needs.  No sort, no reduce, any bucket size
+// (chunks of kE elements in order, running row cursors); a bucket that fits
+// one chunk is staged in shared memory and written out coalesced.
 template <class T>
-__global__ void __launch_bounds__(32 * kFW)
+struct FinishSmem {
+  unsigned wc[kW][sr::kMaxW];  // per-warp row counters -> offsets within the chunk
+  unsigned run[sr::kMaxW];     // row cursors (bucket-local output position)
+  unsigned ctot[sr::kMaxW];    // the chunk's count of each row
+  unsigned rk[kE];             // staged output rows
+  T v[kE];                     // staged output values
+  unsigned long long scan[kT / 32 + 1];
+};
+
+template <class T>
+__global__ void __launch_bounds__(kT, 3)
 ln_transpose_finish_kernel(long long nb, const unsigned* __restrict__ bstart, const unsigned* __restrict__ bK,
                            const T* __restrict__ bV, const unsigned* __restrict__ cbcol, int mb, long long n_out_cols,
                            int* __restrict__ col_ptr, int* __restrict__ row_idx, T* __restrict__ out_vals,
                            long long* info) {
-  __shared__ unsigned cur_s[kFW][sr::kMaxW];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned* cur = cur_s[warp];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FinishSmem<T>& S = *reinterpret_cast<FinishSmem<T>*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned mmask = mb >= 32 ? 0xffffffffu : ((1u << mb) - 1u);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && tid == 0) {
     const unsigned n = __ldg(&bstart[nb]);
     col_ptr[n_out_cols] = (int)n;
     if (info) info[0] = n;
   }
-  constexpr int kB = 8;  // elements per lane per batch
-  for (long long t = (long long)blockIdx.x * kFW + warp; t < nb; t += (long long)gridDim.x * kFW) {
+  for (long long t = blockIdx.x; t < nb; t += gridDim.x) {
     const unsigned s0 = __ldg(&bstart[t]), L = __ldg(&bstart[t + 1]) - s0;
     const unsigned c0 = __ldg(&cbcol[t]);
     const int W = (int)(__ldg(&cbcol[t + 1]) - c0);
-    for (int l = lane; l < W; l += 32) cur[l] = 0u;
-    __syncwarp();
-    for (unsigned base = 0; base < L; base += 32 * kB) {  // counts
-      unsigned key[kB];
+    const bool one = L <= (unsigned)kE;
+    // the first chunk's loads go out before anything waits
+    unsigned key[kI];
+    T v[kI];
 #pragma unroll
-      for (int k = 0; k < kB; k++) {
-        const unsigned i = base + k * 32 + lane;
-        key[k] = i < L ? __ldcs(&bK[s0 + i]) : 0xffffffffu;
+    for (int k = 0; k < kI; k++) {
+      const unsigned i = warp * (32 * kI) + k * 32 + lane;
+      if (i < L) {
+        key[k] = __ldcs(&bK[s0 + i]);
+        v[k] = __ldcs(&bV[s0 + i]);
       }
-#pragma unroll
-      for (int k = 0; k < kB; k++)
-        if (key[k] != 0xffffffffu) atomicAdd(&cur[key[k] >> mb], 1u);
     }
-    __syncwarp();
-    {  // exclusive scan of the counts -> row cursors and col_ptr (lane l owns a slice)
-      const int per = (W + 31) / 32, b0 = lane * per;
-      unsigned sum = 0;
-      for (int q = 0; q < per; q++)
-        if (b0 + q < W) sum += cur[b0 + q];
-      const unsigned inc = warp_inclusive_scan(sum);
-      unsigned run = inc - sum;
-      for (int q = 0; q < per; q++) {
-        if (b0 + q < W) {
-          const unsigned c = cur[b0 + q];
-          cur[b0 + q] = run;
-          col_ptr[c0 + b0 + q] = (int)(s0 + run);
+    __syncthreads();  // the previous bucket's shared memory is free
+    for (int l = tid; l < W; l += kT) S.run[l] = 0u;
+    __syncthreads();
+    // row counts of the whole bucket -> row starts (run) and col_ptr
+    if (one) {
+#pragma unroll
+      for (int k = 0; k < kI; k++)
+        if (warp * (32 * kI) + k * 32 + lane < L) atomicAdd(&S.run[key[k] >> mb], 1u);
+    } else {
+      for (unsigned i = tid; i < L; i += kT) atomicAdd(&S.run[__ldcs(&bK[s0 + i]) >> mb], 1u);
+    }
+    __syncthreads();
+    {
+      constexpr int kPerT = (sr::kMaxW + kT - 1) / kT;
+      unsigned c[kPerT], sum = 0;
+#pragma unroll
+      for (int q = 0; q < kPerT; q++) {
+        const int l = tid * kPerT + q;
+        c[q] = l < W ? S.run[l] : 0u;
+        sum += c[q];
+      }
+      unsigned long long tot;
+      unsigned long long ex = block_exclusive_scan<unsigned long long>(sum, S.scan, &tot);
+#pragma unroll
+      for (int q = 0; q < kPerT; q++) {
+        const int l = tid * kPerT + q;
+        if (l < W) {
+          S.run[l] = (unsigned)ex;
+          col_ptr[c0 + l] = (int)(s0 + ex);
+        }
+        ex += c[q];
+      }
+    }
+    for (unsigned base = 0; base < L; base += kE) {  // chunks in input order
+      if (base > 0) {
+#pragma unroll
+        for (int k = 0; k < kI; k++) {
+          const unsigned i = base + warp * (32 * kI) + k * 32 + lane;
+          if (i < L) {
+            key[k] = __ldcs(&bK[s0 + i]);
+            v[k] = __ldcs(&bV[s0 + i]);
+          }
+        }
+      }
+      for (int l = lane; l < W; l += 32) S.wc[warp][l] = 0u;
+      __syncwarp();
+      unsigned rk[kI], lr[kI];
+#pragma unroll
+      for (int k = 0; k < kI; k++) {
+        const bool in = base + warp * (32 * kI) + k * 32 + lane < L;
+        lr[k] = in ? key[k] >> mb : 0xffffffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, lr[k]);
+        unsigned b0 = 0;
+        if (in) b0 = S.wc[warp][lr[k]];
+        rk[k] = b0 + __popc(peers & lanemask_lt());
+        __syncwarp();
+        if (in && (peers & lanemask_lt()) == 0u) S.wc[warp][lr[k]] = b0 + __popc(peers);
+        __syncwarp();
+      }
+      __syncthreads();
+      for (int l = tid; l < W; l += kT) {  // per row: warp offsets (warp order), chunk count
+        unsigned run = 0;
+#pragma unroll
+        for (int w = 0; w < kW; w++) {
+          const unsigned c = S.wc[w][l];
+          S.wc[w][l] = run;
           run += c;
         }
+        S.ctot[l] = run;
       }
-    }
-    __syncwarp();
-    for (unsigned base = 0; base < L; base += 32 * kB) {  // placement in input order
-      unsigned key[kB];
-      T v[kB];
+      __syncthreads();
 #pragma unroll
-      for (int k = 0; k < kB; k++) {
-        const unsigned i = base + k * 32 + lane;
-        key[k] = i < L ? __ldcs(&bK[s0 + i]) : 0xffffffffu;
-        v[k] = i < L ? __ldcs(&bV[s0 + i]) : T(0);
-      }
-#pragma unroll
-      for (int k = 0; k < kB; k++) {
-        const bool in = key[k] != 0xffffffffu;
-        const unsigned lr = in ? key[k] >> mb : 0xffffffffu;
-        const unsigned peers = __match_any_sync(0xffffffffu, lr);
-        const unsigned r = __popc(peers & lanemask_lt());
-        const unsigned start = in ? cur[lr] : 0u;
-        __syncwarp();
-        if (in) {
-          if ((peers & lanemask_lt()) == 0u) cur[lr] = start + __popc(peers);
-          __stcs(&row_idx[s0 + start + r], (int)(key[k] & mmask));
-          __stcs(&out_vals[s0 + start + r], v[k]);
+      for (int k = 0; k < kI; k++) {
+        if (lr[k] == 0xffffffffu) continue;
+        const unsigned p = S.run[lr[k]] + S.wc[warp][lr[k]] + rk[k];  // bucket-local output position
+        if (one) {
+          S.rk[p] = key[k] & mmask;
+          S.v[p] = v[k];
+        } else {
+          __stcs(&row_idx[s0 + p], (int)(key[k] & mmask));
+          __stcs(&out_vals[s0 + p], v[k]);
         }
-        __syncwarp();
+      }
+      __syncthreads();
+      if (one) {
+        for (unsigned q = tid; q < L; q += kT) {
+          __stcs(&row_idx[s0 + q], (int)S.rk[q]);
+          __stcs(&out_vals[s0 + q], S.v[q]);
+        }
+      } else {
+        for (int l = tid; l < W; l += kT) S.run[l] += S.ctot[l];
+        __syncthreads();
       }
     }
-    __syncwarp();
   }
 }
 
