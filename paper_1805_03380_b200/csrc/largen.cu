@@ -181,7 +181,7 @@ static int prepare(CooIn<IdxT, T>&, const Ws<T>&, cudaStream_t) {
 }
 
 template <class T, class In>
-static int run(In src, long long n, long long n_out_cols, int mb, int mode, int prune, int* col_ptr,
+static int run(In src, long long n, long long n_out_cols, int mb, long long n_minor, int mode, int prune, int* col_ptr,
                int* row_idx, T* out_vals, long long* info, void* ws, size_t ws_bytes, cudaStream_t st,
                bool transpose_finish = false) {
   if (disabled()) return -1;
@@ -255,6 +255,7 @@ static int run(In src, long long n, long long n_out_cols, int mb, int mode, int 
   o.mode = mode;
   o.prune = prune;
   o.mb = mb;
+  o.n_minor = n_minor;
   o.idx_bits = bits_for(n > 0 ? n - 1 : 0);
   o.stop = 0;
   o.n_out_cols = n_out_cols;
@@ -283,7 +284,8 @@ int coo_to_csc(long long n_rows, long long n_cols, long long n, const IdxT* rows
                int mode, int* col_ptr, int* row_idx, T* out_vals, long long* info, void* ws, size_t ws_bytes,
                cudaStream_t st) {
   return run<T>(CooIn<IdxT, T>{rows, cols, vals, n, n_rows, n_cols}, n, n_cols,
-                bits_for(n_rows > 0 ? n_rows - 1 : 0), mode, 1, col_ptr, row_idx, out_vals, info, ws, ws_bytes, st);
+                bits_for(n_rows > 0 ? n_rows - 1 : 0), n_rows, mode, 1, col_ptr, row_idx, out_vals, info, ws, ws_bytes,
+                st);
 }
 
 template <class T>
@@ -291,7 +293,7 @@ int transpose(long long n_rows, long long n_cols, long long nnz, const int* col_
               const T* vals, int* t_col_ptr, int* t_row_idx, T* t_vals, void* ws, size_t ws_bytes, cudaStream_t st) {
   static const bool generic = getenv("AS_LN_GENERIC_TRANSPOSE") != nullptr;  // A/B: tile-phase finish
   return run<T>(CscIn<T>{col_ptr, row_idx, vals, n_cols, nnz, nullptr}, nnz, n_rows, bits_for(n_cols > 0 ? n_cols - 1 : 0),
-                kLast, 0, t_col_ptr, t_row_idx, t_vals, nullptr, ws, ws_bytes, st, !generic);
+                n_cols, kLast, 0, t_col_ptr, t_row_idx, t_vals, nullptr, ws, ws_bytes, st, !generic);
 }
 
 template int coo_to_csc<double, int>(long long, long long, long long, const int*, const int*, const double*, int, int*,

@@ -14,14 +14,14 @@ int coo_to_csc(long long n_rows, long long n_cols, long long n, const IdxT* rows
                int mode, int* col_ptr, int* row_idx, T* out_vals, long long* info, void* ws, size_t ws_bytes,
                cudaStream_t st) {
   return run<T>(Coo<IdxT, T>{rows, cols, vals, n, n_rows, n_cols}, None{}, n, n, n_cols,
-                bits_for(n_rows > 0 ? n_rows - 1 : 0), mode, 1, col_ptr, row_idx, out_vals, info, ws, ws_bytes, st);
+                bits_for(n_rows > 0 ? n_rows - 1 : 0), n_rows, mode, 1, col_ptr, row_idx, out_vals, info, ws, ws_bytes, st);
 }
 
 template <class T>
 int transpose(long long n_rows, long long n_cols, long long nnz, const int* col_ptr, const int* row_idx,
               const T* vals, int* t_col_ptr, int* t_row_idx, T* t_vals, void* ws, size_t ws_bytes, cudaStream_t st) {
   return run<T>(Csc<T>{col_ptr, row_idx, vals, n_cols, nnz, true}, None{}, nnz, nnz, n_rows,
-                bits_for(n_cols > 0 ? n_cols - 1 : 0), kLast, 0, t_col_ptr, t_row_idx, t_vals, nullptr, ws, ws_bytes,
+                bits_for(n_cols > 0 ? n_cols - 1 : 0), n_cols, kLast, 0, t_col_ptr, t_row_idx, t_vals, nullptr, ws, ws_bytes,
                 st);
 }
 
@@ -31,7 +31,7 @@ int flush_f64(long long n_rows, long long n_cols, long long nnz_base, const int*
               size_t ws_bytes, cudaStream_t st) {
   return run<double>(Csc<double>{base_col_ptr, base_row_idx, base_vals, n_cols, nnz_base, false},
                      Coo<int, double>{log_rows, log_cols, log_vals, n_log, n_rows, n_cols}, nnz_base, nnz_base + n_log,
-                     n_cols, bits_for(n_rows > 0 ? n_rows - 1 : 0), kLast, 1, col_ptr, row_idx, out_vals, info, ws,
+                     n_cols, bits_for(n_rows > 0 ? n_rows - 1 : 0), n_rows, kLast, 1, col_ptr, row_idx, out_vals, info, ws,
                      ws_bytes, st);
 }
 

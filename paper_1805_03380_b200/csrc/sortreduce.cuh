@@ -55,6 +55,10 @@ constexpr int kTP = kTile / kThreads;          // tile elements per thread
 constexpr int kNB = AS_SR_NB;                  // bins per tile
 constexpr int kMaxW = 1024;                    // columns per bucket
 constexpr int kRankMax = 32;                   // bins up to this rank by counting
+#ifndef AS_SR_RANK_UNROLL
+#define AS_SR_RANK_UNROLL 1
+#endif
+constexpr int kRankUnroll = AS_SR_RANK_UNROLL;  // unroll of the in-bin rank loop
 constexpr int kColCache = 1024;                // CSC source: cached column pointers of a chunk
 constexpr int kMaxCb = 4096;                   // buckets (shared-memory tables)
 constexpr int kRankBits = 12;                  // P1 rank in (CTA, bucket): < kChunkMax
@@ -93,6 +97,7 @@ struct Args {
   long long n1, n;                 // elements of s1; of s1 ++ s2
   long long n_out_cols;            // output columns (major range)
   int minor_bits;
+  long long n_minor;               // minor index range [0, n_minor)
   long long ncb;
   unsigned long long cb_mul;       // bucket(c) = (c * cb_mul) >> 32
   int mode, prune;
@@ -656,6 +661,7 @@ struct SegSR {
 template <class T>
 struct TileOut {
   int mode, prune, mb, idx_bits, stop;
+  long long n_minor;  // minor values in use: [0, n_minor)
   long long n_out_cols;
   int* col_ptr;
   int* row_idx;
@@ -795,10 +801,13 @@ __device__ __forceinline__ void tile_phase(const Seg& sg, const TileOut<T>& o, T
     // are consecutive wherever the layout allows); bins: aligned ranges of the
     // key between 0 and Wt << mb, at most kNB, never wider than one column
     SR_CLK(0, t == g);
-    const unsigned long long range = (unsigned long long)Wt << mb;
+    // bins: bpc per column over the minor range actually used ([0, n_minor),
+    // not the 2^mb the key reserves), each 2^sh minor values wide
+    const unsigned nmin = o.n_minor > 0 ? (unsigned)o.n_minor : 1u;
     int sh = 0;
-    while (((range - 1) >> sh) >= (unsigned long long)kNB) sh++;
-    const int nbins = (int)(((range - 1) >> sh) + 1);
+    while ((unsigned long long)Wt * (((nmin - 1) >> sh) + 1) > (unsigned long long)kNB) sh++;
+    const unsigned bpc = ((nmin - 1) >> sh) + 1;
+    const int nbins = (int)((unsigned)Wt * bpc);
     // staging slot of every element of the tile (the map aliases TK, written later)
     for (unsigned e = 0; e < seglen; e++) S.u.a.TK[segoff + e] = segsrc + e;
     __syncthreads();
@@ -823,7 +832,7 @@ __device__ __forceinline__ void tile_phase(const Seg& sg, const TileOut<T>& o, T
 #pragma unroll
     for (int u = 0; u < kTP; u++) {
       if (tid + u * kThreads < m) {
-        const unsigned b = k4[u] >> sh;
+        const unsigned b = (k4[u] >> mb) * bpc + ((k4[u] & mmask) >> sh);
         br[u] = (b << 16) | atomicAdd(&S.cnt[b], 1u);
       }
     }
@@ -866,8 +875,8 @@ __device__ __forceinline__ void tile_phase(const Seg& sg, const TileOut<T>& o, T
       }
     }
     for (int l = tid; l <= Wt; l += kThreads) {
-      const unsigned long long bl = ((unsigned long long)l << mb) >> sh;
-      S.cstart[l] = (unsigned short)S.bs[bl < (unsigned long long)nbins ? bl : nbins];
+      const unsigned bl = (unsigned)l * bpc;
+      S.cstart[l] = (unsigned short)S.bs[bl < (unsigned)nbins ? bl : (unsigned)nbins];
     }
     __syncthreads();
     SR_CLK(4, t == g);
@@ -883,6 +892,7 @@ __device__ __forceinline__ void tile_phase(const Seg& sg, const TileOut<T>& o, T
           // branch-free count of the bin's (key, index) pairs below this one
           unsigned r = 0;
           const unsigned k = k4[u], x = x4[u];
+#pragma unroll kRankUnroll
           for (unsigned j = b0; j < b1; j++) {
             const unsigned kj = S.u.a.TK[j], xj = S.u.a.TX[j];
             r += (unsigned)(kj < k) | ((unsigned)(kj == k) & (unsigned)(xj < x));
@@ -1220,6 +1230,7 @@ __global__ void __launch_bounds__(kThreads, 2) sortreduce_kernel(Args<T, S1, S2>
     to.mode = a.mode;
     to.prune = a.prune;
     to.mb = a.minor_bits;
+    to.n_minor = a.n_minor;
     to.idx_bits = a.idx_bits;
     to.stop = a.stop;
     to.n_out_cols = a.n_out_cols;

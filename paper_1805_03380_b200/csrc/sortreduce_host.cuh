@@ -122,7 +122,8 @@ inline bool disabled() {
 // Returns AS_OK after launching, or -1 when the input is outside this
 // kernel's envelope (the caller falls back to the general bucket kernel).
 template <class T, class S1, class S2>
-static int run(const S1& s1, const S2& s2, long long n1, long long n, long long n_out_cols, int minor_bits, int mode,
+static int run(const S1& s1, const S2& s2, long long n1, long long n, long long n_out_cols, int minor_bits,
+               long long n_minor, int mode,
                int prune, int* col_ptr, int* row_idx, T* out_vals, long long* info, void* ws, size_t ws_bytes,
                cudaStream_t st) {
   if (disabled()) return -1;
@@ -141,6 +142,7 @@ static int run(const S1& s1, const S2& s2, long long n1, long long n, long long 
   a.n = n;
   a.n_out_cols = n_out_cols;
   a.minor_bits = minor_bits;
+  a.n_minor = n_minor;
   a.ncb = p.ncb;
   a.cb_mul = p.cb_mul;
   a.mode = mode;
