@@ -145,7 +145,7 @@ static int scatter_launch(const Args<T>& a, const In& src, cudaStream_t st) {
   static bool attr[kMaxDevices] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
-  const int smem = (int)sizeof(ScatterSmem<T, kPass>);
+  const int smem = (int)sizeof(ScatterSmem<T, In, kPass>);
   if (dev >= 0 && dev < kMaxDevices && !attr[dev]) {
     AS_CUDA_TRY(cudaFuncSetAttribute(ln_scatter_kernel<T, In, kPass>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      smem));
@@ -206,6 +206,7 @@ static int run(In src, long long n, long long n_out_cols, int mb, long long n_mi
   a.lob = p.lob;
   a.nb = p.nb;
   a.cb_mul = p.cb_mul;
+  a.inv_cb = p.cb_mul ? 1.0 / (double)p.cb_mul : 0.0;
   a.H = w.H;
   a.bcnt = w.bcnt;
   a.cbcol = w.cbcol;

@@ -94,6 +94,7 @@ struct Args {
   T* aV;
   unsigned* bK;                // pass B records (bucket order)
   T* bV;
+  double inv_cb;               // 1.0 / cb_mul (local_col)
 };
 
 AS_DEVICE_INLINE unsigned bucket_of(unsigned maj, unsigned long long cb_mul) {
@@ -102,11 +103,18 @@ AS_DEVICE_INLINE unsigned bucket_of(unsigned maj, unsigned long long cb_mul) {
 
 // column of maj inside its bucket: maj - cbcol[bucket_of(maj)] = floor(f / cb_mul)
 // with f = maj * cb_mul mod 2^32 (moving d columns down stays in the bucket
-// while d * cb_mul <= f); one 32-bit division, no table lookup
-AS_DEVICE_INLINE unsigned local_col(unsigned maj, unsigned long long cb_mul) {
+// while d * cb_mul <= f).  The quotient comes from a double reciprocal
+// (relative error ~2^-52, so it is off by at most one) and one exact integer
+// correction -- no 32-bit division (which was a sixth of the scatter's
+// instructions).
+AS_DEVICE_INLINE unsigned local_col(unsigned maj, unsigned long long cb_mul, double inv_cb) {
   if (cb_mul >> 32) return 0u;  // one column per bucket
   const unsigned f = (unsigned)((unsigned long long)maj * cb_mul);
-  return f / (unsigned)cb_mul;
+  unsigned q = (unsigned)((double)f * inv_cb);
+  const unsigned long long d = cb_mul;
+  if ((unsigned long long)q * d > f) q--;
+  else if ((unsigned long long)(q + 1) * d <= f) q++;
+  return q;
 }
 
 // ---- items: every element of a thread is loaded first (all loads in
@@ -343,7 +351,7 @@ ln_scan_kernel(unsigned* x, long long n, unsigned* out_total, unsigned long long
 
 // ------------------------------------------------------------------------
 // scatter: stable counting sort of tile t by digit into the pass's records
-template <class T, int kPass>
+template <class T, class In, int kPass>
 struct ScatterSmem {
   unsigned wc[kW][kR];      // per-warp digit counters -> per-warp offsets
   unsigned tstart[kR];      // tile-local digit starts
@@ -363,7 +371,7 @@ struct ScatterSmem {
 template <class T, class In, int kPass>
 __global__ void __launch_bounds__(kT, AS_LN_SCATTER_MINB) ln_scatter_kernel(Args<T> a, In src) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ScatterSmem<T, kPass>& S = *reinterpret_cast<ScatterSmem<T, kPass>*>(smem_raw);
+  ScatterSmem<T, In, kPass>& S = *reinterpret_cast<ScatterSmem<T, In, kPass>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long t = blockIdx.x;
   const long long lo = t * kE, hi = min(a.n, lo + kE);
@@ -429,7 +437,7 @@ __global__ void __launch_bounds__(kT, AS_LN_SCATTER_MINB) ln_scatter_kernel(Args
       S.k1[p] = maj;
       S.k2[p] = mn;
     } else {
-      S.k1[p] = (local_col(maj, a.cb_mul) << a.mb) | mn;
+      S.k1[p] = (local_col(maj, a.cb_mul, a.inv_cb) << a.mb) | mn;
     }
     S.v[p] = it.v[k];
     S.d[p] = (unsigned char)dg[k];
