@@ -435,7 +435,7 @@ static AddWs carve_add(void* ws, size_t cap, long long n_tiles, size_t* need) {
 
 // resident CTAs of the persistent tile kernel (per device; 0 = cannot configure)
 static int add_resident() {
-  static int grid[kMaxDevices] = {0};
+  static std::atomic<int> grid[kMaxDevices];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
   if (grid[dev] == 0) {

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -52,12 +53,26 @@ struct Carve {
   }
 };
 
-constexpr int kNumSMs = 148;
 constexpr int kMaxDevices = 64;  // per-device launch-configuration caches
+
+// SM count of the current device (queried once per device; B200: 148).  The
+// per-device caches below and in the launchers are std::atomic: concurrent
+// first calls from several host threads compute the same value.
+inline int num_sms() {
+  static std::atomic<int> sms[kMaxDevices];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 148;
+  int v = sms[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    sms[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
 
 inline int grid_for(long long n, int block, int per_sm = 8) {
   long long g = (n + block - 1) / block;
-  long long cap = (long long)kNumSMs * per_sm;
+  long long cap = (long long)num_sms() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;

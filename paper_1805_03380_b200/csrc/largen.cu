@@ -125,7 +125,7 @@ bool disabled() {
 // co-resident grid of the tile kernel (per device, cached)
 template <class T>
 static int tiles_grid() {
-  static int grid[kMaxDevices] = {0};
+  static std::atomic<int> grid[kMaxDevices];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
   if (grid[dev] == 0) {
@@ -142,7 +142,7 @@ static int tiles_grid() {
 
 template <class T, class In, int kPass>
 static int scatter_launch(const Args<T>& a, const In& src, cudaStream_t st) {
-  static bool attr[kMaxDevices] = {false};
+  static std::atomic<bool> attr[kMaxDevices];
   int dev = 0;
   cudaGetDevice(&dev);
   const int smem = (int)sizeof(ScatterSmem<T, In, kPass>);
@@ -236,7 +236,7 @@ static int run(In src, long long n, long long n_out_cols, int mb, long long n_mi
     if (int rc = scatter_launch<T, In, 2>(a, src, st)) return rc;
   }
   if (mode == kLast && !prune && transpose_finish) {  // every element kept, no duplicates: no sort
-    static bool attr[kMaxDevices] = {false};
+    static std::atomic<bool> attr[kMaxDevices];
     int dev = 0;
     cudaGetDevice(&dev);
     const int smem = (int)sizeof(FinishSmem<T>);

@@ -43,7 +43,7 @@ struct PersistWs {
 
 // Coarse buckets of ~n_cols / n_cb consecutive output columns (bucket(c) =
 // (c * cb_mul) >> 32).  n_cb: ~0.9 * kCap elements per bucket on average,
-// rounded up to whole waves of the co-resident grid (kNumSMs x AS_PERSIST_MINB
+// rounded up to whole waves of the co-resident grid (SMs x AS_PERSIST_MINB
 // CTAs) when above one wave, so the tile phase has no half-empty last wave
 // (AS_FILL / AS_WAVES override, for sweeps); at least n_cols / kMaxBucketCols
 // (a bucket's columns index shared arrays), at most kMaxCoarse.  Returns 0
@@ -52,7 +52,7 @@ constexpr long long kMaxBucketCols = kMaxW - 24;
 
 static inline long long choose_ncb(long long n, long long n_cols) {
   static const double kFill = getenv("AS_FILL") ? atof(getenv("AS_FILL")) : 0.9;
-  const long long wave = (long long)kNumSMs * AS_PERSIST_MINB;
+  const long long wave = (long long)num_sms() * AS_PERSIST_MINB;
   long long nb = (long long)((double)n / (kFill * kCap)) + 1;
   static const int kWaves = getenv("AS_WAVES") ? atoi(getenv("AS_WAVES")) : 1;
   if (kWaves == 2 || (kWaves == 1 && nb > wave)) nb = (nb + wave - 1) / wave * wave;
@@ -116,7 +116,7 @@ static size_t carve_persist(Carve& c, PersistWs* w, long long n, long long n_col
 
 template <class T, class S1, class S2, bool kTwo>
 static int launch_persist_k(PersistArgs<T, S1, S2>& a, cudaStream_t st) {
-  static int grid_of[kMaxDevices] = {0};  // per device: the attribute and occupancy are per device
+  static std::atomic<int> grid_of[kMaxDevices];  // per device: the attribute and occupancy are per device
   const size_t smem = sizeof(PersistSmem<T>);
   auto kern = persist_bucket_kernel<T, S1, S2, kTwo>;
   int dev = 0;

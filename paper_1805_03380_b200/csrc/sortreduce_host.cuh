@@ -98,7 +98,7 @@ static Plan plan(long long n, long long n_out_cols, int minor_bits, int grid) {
 // co-resident grid of the instantiation (per device, cached)
 template <class T, class S1, class S2>
 static int grid_of() {
-  static int grid[kMaxDevices] = {0};
+  static std::atomic<int> grid[kMaxDevices];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
   if (grid[dev] == 0) {

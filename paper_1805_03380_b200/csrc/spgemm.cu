@@ -319,7 +319,7 @@ int as_spgemm_products(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, cons
     spgemm_count_kernel<<<grid_for((n_cols_b + 31) / 32 * 32, kGThreads), kGThreads, 0, st>>>(n_cols_b, a_col_ptr, b_col_ptr,
                                                                              b_row_idx, counts, longs, ticket + 32);
     AS_LAUNCH_CHECK();
-    spgemm_count_long_kernel<<<kNumSMs * 4, kGThreads, 0, st>>>(a_col_ptr, b_col_ptr, b_row_idx, counts, longs,
+    spgemm_count_long_kernel<<<num_sms() * 4, kGThreads, 0, st>>>(a_col_ptr, b_col_ptr, b_row_idx, counts, longs,
                                                                ticket + 32);
     AS_LAUNCH_CHECK();
   }
@@ -389,7 +389,7 @@ int as_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int
     spgemm_range_bounds_kernel<<<grid_for(ranges, kExThreads), kExThreads, 0, st>>>(
         ranges, nnz_b, n_cols_b, total_products, b_col_ptr, ent_ptr, bounds);
     AS_LAUNCH_CHECK();
-    spgemm_expand_kernel<<<(unsigned)std::min<long long>(ranges, (long long)kNumSMs * 32), kExThreads, 0, st>>>(
+    spgemm_expand_kernel<<<(unsigned)std::min<long long>(ranges, (long long)num_sms() * 32), kExThreads, 0, st>>>(
         nnz_b, n_cols_b, total_products, a_col_ptr, a_row_idx, a_vals, b_col_ptr, b_row_idx, b_vals, ent_ptr, bounds,
         (const long long*)prod_ptr, dense ? (long long)kCap : LLONG_MAX, w.keys, w.colb, (double*)w.vals_b);
     AS_LAUNCH_CHECK();

@@ -248,7 +248,7 @@ trace_partial_kernel(long long n_cols, const int* __restrict__ ap, const int* __
 }
 
 static int trace_grid() {
-  static int grid[kMaxDevices] = {0};
+  static std::atomic<int> grid[kMaxDevices];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 148;
   if (grid[dev] == 0) {
