@@ -165,16 +165,24 @@ struct Items<T, CooIn<IdxT, T>> {
     c[k] = __ldcs(&s.cols[e]);
     if (kVal) v[k] = __ldcs(&s.vals[e]);
   }
-  // false: an out-of-range triplet (skipped; its index goes to *bad)
+  // false: an out-of-range triplet (skipped; its index goes to *bad).  int32
+  // indices compare unsigned (a negative index wraps above any dimension)
   AS_DEVICE_INLINE bool major(const CooIn<IdxT, T>& s, int k, long long e, unsigned& maj, unsigned long long* bad) {
-    const long long rr = (long long)r[k], cc = (long long)c[k];
-    if (rr < 0 || rr >= s.n_rows || cc < 0 || cc >= s.n_cols) {
+    bool ok;
+    if constexpr (sizeof(IdxT) == 4) {
+      ok = (unsigned)r[k] < (unsigned)s.n_rows && (unsigned)c[k] < (unsigned)s.n_cols;
+    } else {
+      ok = (unsigned long long)r[k] < (unsigned long long)s.n_rows &&
+           (unsigned long long)c[k] < (unsigned long long)s.n_cols;
+    }
+    if (!ok) {
       if (bad) atomicMin(bad, (unsigned long long)e);
       return false;
     }
-    maj = (unsigned)cc;
+    maj = (unsigned)c[k];
     return true;
   }
+  AS_DEVICE_INLINE unsigned maj_raw(int k) const { return (unsigned)c[k]; }  // (already validated)
   AS_DEVICE_INLINE unsigned minor(const CooIn<IdxT, T>&, int k, long long, const ColCache&, const int*) {
     return (unsigned)r[k];
   }
@@ -206,6 +214,7 @@ struct Items<T, CscIn<T>> {
     maj = (unsigned)i[k];
     return true;
   }
+  AS_DEVICE_INLINE unsigned maj_raw(int k) const { return (unsigned)i[k]; }
   AS_DEVICE_INLINE unsigned minor(const CscIn<T>& s, int, long long e, const ColCache& cc, const int* colc) {
     if (cur < 0) {  // first element: binary search
       if (cc.nc >= 0) {
@@ -245,6 +254,7 @@ struct Items<T, RecIn<T>> {
     maj = m[k];
     return true;
   }
+  AS_DEVICE_INLINE unsigned maj_raw(int k) const { return m[k]; }
   AS_DEVICE_INLINE unsigned minor(const RecIn<T>&, int k, long long, const ColCache&, const int*) { return n[k]; }
 };
 
@@ -353,7 +363,7 @@ ln_scan_kernel(unsigned* x, long long n, unsigned* out_total, unsigned long long
 // scatter: stable counting sort of tile t by digit into the pass's records
 template <class T, class In, int kPass>
 struct ScatterSmem {
-  unsigned wc[kW][kR];      // per-warp digit counters -> per-warp offsets
+  alignas(16) unsigned wc[kW][kR];  // per-warp digit counters -> per-warp offsets
   unsigned tstart[kR];      // tile-local digit starts
   unsigned gbase[kR];       // global start of the tile's run of each digit
   unsigned k1[kE];          // major (pass A) or bucket-local key
@@ -383,7 +393,8 @@ __global__ void __launch_bounds__(kT, AS_LN_SCATTER_MINB) ln_scatter_kernel(Args
     const long long e = elem_of(t, k);
     if (e < hi) it.template fetch<true>(src, k, e);
   }
-  for (int i = lane; i < kR; i += 32) S.wc[warp][i] = 0u;
+  reinterpret_cast<uint4*>(S.wc[warp])[lane] = make_uint4(0u, 0u, 0u, 0u);  // 256 counters: 2 x 16 B per lane
+  reinterpret_cast<uint4*>(S.wc[warp])[lane + 32] = make_uint4(0u, 0u, 0u, 0u);
   it.prep(src, lo, hi, S.colc, &S.cc);  // (CSC source: the tile's column pointers; syncs)
   __syncthreads();
   const ColCache cc = S.cc;
@@ -430,8 +441,7 @@ __global__ void __launch_bounds__(kT, AS_LN_SCATTER_MINB) ln_scatter_kernel(Args
     if (dg[k] == 0xffffu) continue;
     const long long e = elem_of(t, k);
     const unsigned p = S.tstart[dg[k]] + S.wc[warp][dg[k]] + rk[k];
-    unsigned maj = 0;
-    it.major(src, k, e, maj, nullptr);
+    const unsigned maj = it.maj_raw(k);
     const unsigned mn = it.minor(src, k, e, cc, S.colc);
     if (kPass == 0) {
       S.k1[p] = maj;

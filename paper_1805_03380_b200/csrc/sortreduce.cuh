@@ -804,8 +804,10 @@ __device__ __forceinline__ void tile_phase(const Seg& sg, const TileOut<T>& o, T
     // bins: bpc per column over the minor range actually used ([0, n_minor),
     // not the 2^mb the key reserves), each 2^sh minor values wide
     const unsigned nmin = o.n_minor > 0 ? (unsigned)o.n_minor : 1u;
-    int sh = 0;
-    while ((unsigned long long)Wt * (((nmin - 1) >> sh) + 1) > (unsigned long long)kNB) sh++;
+    // smallest sh with Wt * ceil(nmin / 2^sh) <= kNB: 2^sh >= ceil(nmin / (kNB / Wt))
+    const unsigned bpc_max = (unsigned)kNB / (unsigned)max(Wt, 1);
+    const unsigned xq = (nmin + bpc_max - 1) / bpc_max;
+    const int sh = xq <= 1u ? 0 : 32 - __clz(xq - 1u);
     const unsigned bpc = ((nmin - 1) >> sh) + 1;
     const int nbins = (int)((unsigned)Wt * bpc);
     // staging slot of every element of the tile (the map aliases TK, written later)
@@ -1095,7 +1097,15 @@ __global__ void __launch_bounds__(kThreads, 2) sortreduce_kernel(Args<T, S1, S2>
   unsigned* st_key = reinterpret_cast<unsigned*>(smem + LC.st_key);
   unsigned short* st_idx = reinterpret_cast<unsigned short*>(smem + LC.st_idx);  // local input index
   for (long long t = tid; t <= ncb; t += kThreads) {
-    const unsigned long long c0 = cb_mul ? (((unsigned long long)t << 32) + cb_mul - 1) / cb_mul : 0ull;
+    // first column of bucket t = ceil(t 2^32 / cb_mul): a double quotient (off by
+    // at most one) and exact integer corrections instead of a 64-bit division
+    unsigned long long c0 = 0ull;
+    if (cb_mul) {
+      const unsigned long long num = (unsigned long long)t << 32;
+      c0 = (unsigned long long)((double)num / (double)cb_mul);
+      while (c0 * cb_mul < num) c0++;
+      while (c0 > 0 && (c0 - 1) * cb_mul >= num) c0--;
+    }
     cbcol[t] = (unsigned)(t == ncb ? a.n_out_cols : min((long long)c0, a.n_out_cols));
   }
   for (long long b = tid; b < ncb; b += kThreads) hist[b] = 0u;
