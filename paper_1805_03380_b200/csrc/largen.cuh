@@ -329,17 +329,24 @@ ln_scan_kernel(unsigned* x, long long n, unsigned* out_total, unsigned long long
   __shared__ long long tmp[kScanT / 32 + 1];
   __shared__ long long s_tile;
   __shared__ unsigned long long s_prefix;
+  __shared__ unsigned sx[kScanN + kScanN / 32];  // the tile, moved through shared memory (coalesced I/O)
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const long long t = s_tile;
   constexpr int kPer = kScanN / kScanT;
-  const long long base = t * kScanN + (long long)threadIdx.x * kPer;
+  const long long t0 = t * kScanN;
+  auto pad = [](int i) { return i + (i >> 5); };
+#pragma unroll
+  for (int k = 0; k < kPer; k++) {
+    const int q = k * kScanT + threadIdx.x;
+    sx[pad(q)] = t0 + q < n ? x[t0 + q] : 0u;
+  }
+  __syncthreads();
   unsigned v[kPer];
   long long sum = 0;
 #pragma unroll
   for (int k = 0; k < kPer; k++) {
-    const long long i = base + k;
-    v[k] = i < n ? x[i] : 0u;
+    v[k] = sx[pad(threadIdx.x * kPer + k)];
     sum += v[k];
   }
   long long total;
@@ -352,9 +359,14 @@ ln_scan_kernel(unsigned* x, long long n, unsigned* out_total, unsigned long long
   long long run = (long long)s_prefix + off;
 #pragma unroll
   for (int k = 0; k < kPer; k++) {
-    const long long i = base + k;
-    if (i < n) x[i] = (unsigned)run;
+    sx[pad(threadIdx.x * kPer + k)] = (unsigned)run;
     run += v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kPer; k++) {
+    const int q = k * kScanT + threadIdx.x;
+    if (t0 + q < n) x[t0 + q] = sx[pad(q)];
   }
   if (t == gridDim.x - 1 && threadIdx.x == 0 && out_total) *out_total = (unsigned)((long long)s_prefix + total);
 }

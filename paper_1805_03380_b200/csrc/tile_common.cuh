@@ -102,23 +102,34 @@ AS_DEVICE_INLINE int next_bit(const unsigned* bits, int p, int lim) {
 }
 
 // exclusive scan counts[0..n) -> seg_ptr[0..n] (int64) and zero counts (so
-// they can serve as fill cursors).  Chained scan, 4096 counts per tile.
+// they can serve as fill cursors).  Chained scan, 4096 counts per tile; the
+// tile moves through shared memory so every global access is coalesced (each
+// thread scans 16 consecutive counts: reading them straight from global memory
+// made every warp access touch 32 sectors).
 constexpr int kScanThreads = 256, kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+AS_DEVICE_INLINE int scan_pad(int i) { return i + (i >> 5); }
 static __global__ void __launch_bounds__(kScanThreads)
 count_scan_kernel(unsigned* counts, long long n, long long* seg_ptr, unsigned long long* states, unsigned* ticket) {
   __shared__ long long tmp[kScanThreads / 32 + 1];
   __shared__ long long s_tile;
   __shared__ unsigned long long s_prefix;
+  __shared__ long long sx[kScanTile + kScanTile / 32];
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const long long t = s_tile;
-  const long long base = t * (kScanThreads * kScanItems) + (long long)threadIdx.x * kScanItems;
+  const long long t0 = t * kScanTile;
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++) {
+    const int q = k * kScanThreads + threadIdx.x;
+    sx[scan_pad(q)] = t0 + q < n ? (long long)counts[t0 + q] : 0ll;
+  }
+  __syncthreads();
   unsigned v[kScanItems];
   long long sum = 0;
 #pragma unroll
   for (int k = 0; k < kScanItems; k++) {
-    long long i = base + k;
-    v[k] = i < n ? counts[i] : 0u;
+    v[k] = (unsigned)sx[scan_pad(threadIdx.x * kScanItems + k)];
     sum += v[k];
   }
   long long total;
@@ -131,12 +142,17 @@ count_scan_kernel(unsigned* counts, long long n, long long* seg_ptr, unsigned lo
   long long run = (long long)s_prefix + off;
 #pragma unroll
   for (int k = 0; k < kScanItems; k++) {
-    long long i = base + k;
-    if (i < n) {
-      seg_ptr[i] = run;
-      counts[i] = 0u;
-    }
+    sx[scan_pad(threadIdx.x * kScanItems + k)] = run;
     run += v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++) {
+    const int q = k * kScanThreads + threadIdx.x;
+    if (t0 + q < n) {
+      seg_ptr[t0 + q] = sx[scan_pad(q)];
+      counts[t0 + q] = 0u;
+    }
   }
   if (t == gridDim.x - 1 && threadIdx.x == 0) {
     seg_ptr[n] = (long long)s_prefix + total;
