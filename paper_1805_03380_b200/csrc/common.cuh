@@ -279,12 +279,15 @@ __device__ T pw_sum(Get get, long long off, long long n) {
   }
 }
 
-template <class T, class Get>
+// kSeqOnly: an instantiation that only ever folds sequentially (SpGEMM's
+// pre-bucketed mode) -- the pairwise summation and its explicit stack are not
+// compiled in (they were most of that kernel's 1 KB stack frame)
+template <class T, class Get, bool kSeqOnly = false>
 __device__ T reduce_run(Get get, long long n, int mode) {
   if (mode == kLast) return get(n - 1);
   T v0 = get(0);
   if (n == 1) return v0;
-  if (mode == kSumSeq) {
+  if (kSeqOnly || mode == kSumSeq) {
     T acc = v0;
     for (long long i = 1; i < n; i++) acc = acc + get(i);
     return acc;

@@ -270,6 +270,10 @@ constexpr int kMaxW = 1024;       // columns per coarse bucket
 #endif
 constexpr int kTBins = AS_TBINS;  // second-level bins per bucket tile
 
+// the pre-bucketed instantiation (SpGEMM's reduce, always kSumSeq)
+template <class T, class S1, class S2>
+constexpr bool kPreOnly = std::is_same<S1, NoSrc<T>>::value && std::is_same<S2, NoSrc<T>>::value;
+
 template <class T, class S1, class S2>
 struct PersistArgs {
   S1 s1;
@@ -478,7 +482,7 @@ static __device__ void block_radix_sort_kv(unsigned long long* k, unsigned* p, u
 // the chunk is the whole bucket).  vslot: values by tile slot through S.perm
 // (nullptr: values by input index).  Leaves S.u.rv[p] = run value at kept
 // heads, S.v.excl[0..cm] exclusive kept counts; returns the chunk total.
-template <class T, class VS>
+template <class T, class VS, bool kSeqOnly = false>
 __device__ long long bucket_chunk_reduce(BTileSmem<T>& S, long long b, int cm, long long m,
                                          const unsigned long long* gk, const unsigned* gcol, unsigned col_base,
                                          VS vs, int mode, int prune, const T* vslot) {
@@ -520,7 +524,8 @@ __device__ long long bucket_chunk_reduce(BTileSmem<T>& S, long long b, int cm, l
           v = S.u.rv[p];
         } else {
           const T* rvp = S.u.rv + p;
-          v = reduce_run<T>([&](long long i) -> T { return rvp[i]; }, q - p, mode);
+          auto get = [&](long long i) -> T { return rvp[i]; };
+          v = reduce_run<T, decltype(get), kSeqOnly>(get, q - p, mode);
         }
       } else {
         const unsigned row = key_row(S.sk[p]), col = S.scol[p] + col_base;
@@ -529,9 +534,10 @@ __device__ long long bucket_chunk_reduce(BTileSmem<T>& S, long long b, int cm, l
         const T* rvp = S.u.rv + p;
         const long long in_chunk = cm - p;
         const unsigned long long* gkp = gk + b + p;
-        v = reduce_run<T>(
-            [&](long long i) -> T { return i < in_chunk ? rvp[i] : vs((unsigned long long)key_idx(gkp[i])); },
-            qg - (b + p), mode);
+        auto get = [&](long long i) -> T {
+          return i < in_chunk ? rvp[i] : vs((unsigned long long)key_idx(gkp[i]));
+        };
+        v = reduce_run<T, decltype(get), kSeqOnly>(get, qg - (b + p), mode);
       }
       if (!prune || v != T(0)) {
         f = 1;
@@ -784,7 +790,7 @@ __device__ long long process_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1
       }
       __syncthreads();
       sort_bucket_smem(S, (int)L, W, a.row_bits);
-      const long long ctot = bucket_chunk_reduce<T>(S, 0, (int)L, L, nullptr, nullptr, col_base, a.vs, a.mode,
+      const long long ctot = bucket_chunk_reduce<T, decltype(a.vs), kPreOnly<T, S1, S2>>(S, 0, (int)L, L, nullptr, nullptr, col_base, a.vs, a.mode,
                                                     a.prune, nullptr);
       for (int p = tid; p < L; p += nthr) {
         const unsigned x0 = S.v.excl[p], x1 = S.v.excl[p + 1];
@@ -822,7 +828,7 @@ __device__ long long process_oversized_bucket(BTileSmem<T>& S, PersistArgs<T, S1
           S.scol[i] = (unsigned short)(bc2[b + i] - col_base);
         }
         __syncthreads();
-        const long long ctot = bucket_chunk_reduce<T>(S, b, cm, L, bk2, bc2, col_base, a.vs, a.mode, a.prune,
+        const long long ctot = bucket_chunk_reduce<T, decltype(a.vs), kPreOnly<T, S1, S2>>(S, b, cm, L, bk2, bc2, col_base, a.vs, a.mode, a.prune,
                                                       nullptr);
         for (int p = tid; p < cm; p += nthr) {
           const unsigned x0 = S.v.excl[p], x1 = S.v.excl[p + 1];
@@ -857,7 +863,7 @@ __device__ long long pre_tile_to_tmp(BTileSmem<T>& S, PersistArgs<T, S1, S2>& a,
   }
   __syncthreads();
   sort_bucket_smem(S, m, Wt, a.row_bits);
-  bucket_chunk_reduce<T>(S, 0, m, m, nullptr, nullptr, col_base, a.vs, a.mode, a.prune, a.vals_b + s);
+  bucket_chunk_reduce<T, decltype(a.vs), kPreOnly<T, S1, S2>>(S, 0, m, m, nullptr, nullptr, col_base, a.vs, a.mode, a.prune, a.vals_b + s);
   for (int p = tid; p < m; p += nthr) {
     const unsigned e0 = S.v.excl[p], e1 = S.v.excl[p + 1];
     if (e1 != e0) {
@@ -1520,7 +1526,7 @@ __global__ void __launch_bounds__(kSegThreads, AS_PERSIST_MINB) persist_bucket_k
       __syncthreads();
       tt_mark(1);
       sort_bucket_smem(S, (int)m, Wt, a.row_bits);
-      bucket_chunk_reduce<T>(S, 0, (int)m, m, nullptr, nullptr, col_base, a.vs, a.mode, a.prune, a.vals_b + s);
+      bucket_chunk_reduce<T, decltype(a.vs), kPreOnly<T, S1, S2>>(S, 0, (int)m, m, nullptr, nullptr, col_base, a.vs, a.mode, a.prune, a.vals_b + s);
       if constexpr (kPre) {
         for (int p = tid; p < m; p += nthr) {
           const unsigned e0 = S.v.excl[p], e1 = S.v.excl[p + 1];
