@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(kT, AS_LN_SCATTER_MINB) ln_scatter_kernel(Args
 // split evenly over the CTA's threads; slot = input order; chained look-back
 template <class T>
 struct SegLN {
+  static constexpr bool kContig = true;  // bucket t = slots [bstart[t], bstart[t+1])
   const unsigned* bstart;
   const unsigned* bK;
   const T* bV;
@@ -497,6 +498,7 @@ struct SegLN {
     len = o < L ? min(per, L - o) : 0u;
     src = s0 + o;
   }
+  __device__ __forceinline__ unsigned base(long long t) const { return __ldg(&bstart[t]); }
   __device__ __forceinline__ unsigned key(unsigned s) const { return __ldcs(&bK[s]); }
   __device__ __forceinline__ unsigned idx(unsigned s) const { return s; }
   __device__ __forceinline__ const T* val(unsigned s) const { return bV + s; }

@@ -620,6 +620,7 @@ __device__ inline void block_radix_sort_sr(unsigned long long* k, unsigned* p, u
 // gK[j * ch + loffT[t][j] ...]; prefix by the group look-back
 template <class T>
 struct SegSR {
+  static constexpr bool kContig = false;
   const unsigned* loffT;
   long long G, ch, ncb;
   const unsigned* gK;
@@ -810,15 +811,21 @@ __device__ __forceinline__ void tile_phase(const Seg& sg, const TileOut<T>& o, T
     const int sh = xq <= 1u ? 0 : 32 - __clz(xq - 1u);
     const unsigned bpc = ((nmin - 1) >> sh) + 1;
     const int nbins = (int)((unsigned)Wt * bpc);
-    // staging slot of every element of the tile (the map aliases TK, written later)
-    for (unsigned e = 0; e < seglen; e++) S.u.a.TK[segoff + e] = segsrc + e;
-    __syncthreads();
+    // staging slot of every element of the tile (the map aliases TK, written
+    // later); a contiguous bucket (large-input pipeline) needs no map
+    unsigned cbase = 0;
+    if constexpr (Seg::kContig) {
+      cbase = sg.base(t);
+    } else {
+      for (unsigned e = 0; e < seglen; e++) S.u.a.TK[segoff + e] = segsrc + e;
+      __syncthreads();
+    }
     unsigned k4[kTP], x4[kTP], br[kTP];
 #pragma unroll
     for (int u = 0; u < kTP; u++) {
       const int i = tid + u * kThreads;
       if (i < m) {
-        const unsigned src = S.u.a.TK[i];
+        const unsigned src = Seg::kContig ? cbase + (unsigned)i : S.u.a.TK[i];
         k4[u] = sg.key(src);
         x4[u] = sg.idx(src);
         const unsigned d = (unsigned)__cvta_generic_to_shared(&S.u.a.V[i]);
