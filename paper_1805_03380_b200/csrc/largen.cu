@@ -135,7 +135,7 @@ static int tiles_grid() {
     int per_sm = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ln_tiles_kernel<T>, sr::kThreads, smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid[dev] = std::min(per_sm, 2) * sms;
+    grid[dev] = std::min(per_sm, sr::kMinBlocks) * sms;
   }
   return grid[dev];
 }

@@ -509,7 +509,7 @@ struct SegLN {
 };
 
 template <class T>
-__global__ void __launch_bounds__(sr::kThreads, 2)
+__global__ void __launch_bounds__(sr::kThreads, sr::kMinBlocks)
 ln_tiles_kernel(SegLN<T> sg_, sr::TileOut<T> o_, long long nb, const unsigned long long* bad, long long n) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SegLN<T> sg;

@@ -44,13 +44,25 @@
 namespace as {
 namespace sr {
 
-constexpr int kThreads = 512;
+// CTA shape (experiments: AS_SR_THREADS / AS_SR_TILE / AS_SR_MINB; measured
+// best: 512 threads, 2048-element tiles, 2 CTAs per SM)
+#ifndef AS_SR_THREADS
+#define AS_SR_THREADS 512
+#endif
+#ifndef AS_SR_TILE
+#define AS_SR_TILE 2048
+#endif
+#ifndef AS_SR_MINB
+#define AS_SR_MINB 2
+#endif
+constexpr int kThreads = AS_SR_THREADS;
+constexpr int kMinBlocks = AS_SR_MINB;         // co-resident CTAs per SM
 constexpr int kPer = 8;                        // P1: elements per thread (two groups of 4)
 constexpr int kChunkMax = kThreads * kPer;     // elements per CTA chunk
-constexpr int kTile = 2048;                    // elements of a shared-memory tile
+constexpr int kTile = AS_SR_TILE;              // elements of a shared-memory tile
 constexpr int kTP = kTile / kThreads;          // tile elements per thread
 #ifndef AS_SR_NB
-#define AS_SR_NB 1024
+#define AS_SR_NB (AS_SR_TILE / 2)
 #endif
 constexpr int kNB = AS_SR_NB;                  // bins per tile
 constexpr int kMaxW = 1024;                    // columns per bucket
@@ -1067,7 +1079,7 @@ __device__ __forceinline__ void tile_phase(const Seg& sg, const TileOut<T>& o, T
 
 // ------------------------------------------------------------------------
 template <class T, class S1, class S2>
-__global__ void __launch_bounds__(kThreads, 2) sortreduce_kernel(Args<T, S1, S2> a_) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) sortreduce_kernel(Args<T, S1, S2> a_) {
   extern __shared__ __align__(16) unsigned char smem[];
   // the arguments live in shared memory: kernel-parameter loads go through
   // the constant cache, which shares the SM's L1.5 with instructions and

@@ -13,8 +13,8 @@
 namespace as {
 namespace sr {
 
-constexpr size_t kSmemMax = 112 * 1024;  // per CTA: two CTAs per SM
-constexpr long long kGridMax = 148 * 2;  // workspace bound (per-CTA scratch)
+constexpr size_t kSmemMax = (224 / kMinBlocks) * 1024;  // per CTA: kMinBlocks CTAs per SM
+constexpr long long kGridMax = 148 * kMinBlocks;        // workspace bound (per-CTA scratch)
 
 struct Ws {
   unsigned* loffT;
@@ -108,7 +108,7 @@ static int grid_of() {
     int per_sm = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, kSmemMax);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    static const int kCtas = getenv("AS_SR_CTAS") ? atoi(getenv("AS_SR_CTAS")) : 2;
+    static const int kCtas = getenv("AS_SR_CTAS") ? atoi(getenv("AS_SR_CTAS")) : kMinBlocks;
     grid[dev] = (int)std::min<long long>((long long)std::min(per_sm, kCtas) * sms, kGridMax);
   }
   return grid[dev];
