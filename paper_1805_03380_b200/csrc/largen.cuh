@@ -577,6 +577,72 @@ ln_transpose_finish_kernel(long long nb, const unsigned* __restrict__ bstart, co
       }
     }
     __syncthreads();  // the previous bucket's shared memory is free
+    if (one) {
+      // one chunk (the common case): the per-warp ranks come first, and the
+      // rows' totals from them -- no separate counting pass
+      for (int l = lane; l < W; l += 32) S.wc[warp][l] = 0u;
+      __syncwarp();
+      unsigned rk[kI], lr[kI];
+#pragma unroll
+      for (int k = 0; k < kI; k++) {
+        const bool in = warp * (32 * kI) + k * 32 + lane < L;
+        lr[k] = in ? key[k] >> mb : 0xffffffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, lr[k]);
+        unsigned b0 = 0;
+        if (in) b0 = S.wc[warp][lr[k]];
+        rk[k] = b0 + __popc(peers & lanemask_lt());
+        __syncwarp();
+        if (in && (peers & lanemask_lt()) == 0u) S.wc[warp][lr[k]] = b0 + __popc(peers);
+        __syncwarp();
+      }
+      __syncthreads();
+      for (int l = tid; l < W; l += kT) {  // per row: warp offsets (warp order), total
+        unsigned run = 0;
+#pragma unroll
+        for (int w = 0; w < kW; w++) {
+          const unsigned c = S.wc[w][l];
+          S.wc[w][l] = run;
+          run += c;
+        }
+        S.run[l] = run;
+      }
+      __syncthreads();
+      {
+        constexpr int kPerT = (sr::kMaxW + kT - 1) / kT;
+        unsigned c[kPerT], sum = 0;
+#pragma unroll
+        for (int q = 0; q < kPerT; q++) {
+          const int l = tid * kPerT + q;
+          c[q] = l < W ? S.run[l] : 0u;
+          sum += c[q];
+        }
+        unsigned long long tot;
+        unsigned long long ex = block_exclusive_scan<unsigned long long>(sum, S.scan, &tot);
+#pragma unroll
+        for (int q = 0; q < kPerT; q++) {
+          const int l = tid * kPerT + q;
+          if (l < W) {
+            S.run[l] = (unsigned)ex;
+            col_ptr[c0 + l] = (int)(s0 + ex);
+          }
+          ex += c[q];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kI; k++) {
+        if (lr[k] == 0xffffffffu) continue;
+        const unsigned p = S.run[lr[k]] + S.wc[warp][lr[k]] + rk[k];
+        S.rk[p] = key[k] & mmask;
+        S.v[p] = v[k];
+      }
+      __syncthreads();
+      for (unsigned q = tid; q < L; q += kT) {
+        __stcs(&row_idx[s0 + q], (int)S.rk[q]);
+        __stcs(&out_vals[s0 + q], S.v[q]);
+      }
+      continue;
+    }
     for (int l = tid; l < W; l += kT) S.run[l] = 0u;
     __syncthreads();
     // row counts of the whole bucket -> row starts (run) and col_ptr
