@@ -159,3 +159,44 @@ def test_large_transpose_involution_10m():
     pp, rr, vv = _kernels.transpose(n, n, tp, tr, tv)
     assert torch.equal(pp, p) and torch.equal(rr, r) and torch.equal(vv, v)
     assert torch.equal((tp[1:] - tp[:-1]).long(), torch.bincount(r.long(), minlength=n))
+
+
+def test_flush_beyond_single_launch_envelope():
+    # base CSC (1M nnz) ++ 1.5M element writes (overwrites of base entries, of
+    # earlier writes, and 0.0 erasures): more elements than the single-launch
+    # kernel takes, so the general bucket kernel runs (rbt.to_csc semantics)
+    rng = np.random.default_rng(19)
+    n_rows, n_cols = 400_000, 300_000
+    base = oracle.canonicalize(n_rows, n_cols, rng.integers(0, n_rows, 1_000_000), rng.integers(0, n_cols, 1_000_000),
+                               rng.uniform(-1, 1, 1_000_000))
+    nl = 1_500_000
+    lr = rng.integers(0, n_rows, nl)
+    lc = rng.integers(0, n_cols, nl)
+    bc = np.repeat(np.arange(n_cols), np.diff(base[2]))
+    pick = rng.integers(0, base[1].shape[0], nl // 10)  # overwrite existing entries
+    lr[: nl // 10], lc[: nl // 10] = base[1][pick], bc[pick]
+    lr[-nl // 20:], lc[-nl // 20:] = lr[: nl // 20], lc[: nl // 20]  # rewrite earlier writes
+    lv = rng.uniform(-1, 1, nl)
+    lv[rng.integers(0, nl, nl // 50)] = 0.0  # erasures
+    b = (_dev(base[2], torch.int32), _dev(base[1], torch.int32), _dev(base[0], torch.float64))
+    p, r, v, bad = _kernels.flush_log(n_rows, n_cols, b, _dev(lr, torch.int32), _dev(lc, torch.int32),
+                                      _dev(lv, torch.float64))
+    assert bad is None
+    want = oracle.flush(n_rows, n_cols, base, lr, lc, lv)
+    assert np.array_equal(p.cpu().numpy().astype(np.int64), want[2])
+    assert np.array_equal(r.cpu().numpy().astype(np.int64), want[1])
+    assert np.array_equal(v.cpu().numpy(), want[0])
+
+
+@pytest.mark.parametrize("dup", ["sum", "last"])
+def test_general_bucket_kernel_engine(engine, dup):
+    # engine 2: the general bucket kernel (persist.cuh) for construction and transpose
+    engine(2)
+    rng = np.random.default_rng(20)
+    rows, cols, vals = _with_dups(rng, 50_000, 40_000, 600_000)
+    _check_build(50_000, 40_000, rows, cols, vals, dup)
+    A = oracle.canonicalize(50_000, 40_000, rows, cols, vals)
+    tp, tr, tv = _kernels.transpose(50_000, 40_000, _dev(A[2], torch.int32), _dev(A[1], torch.int32),
+                                    _dev(A[0], torch.float64))
+    want = oracle.transpose(50_000, 40_000, *A)
+    assert np.array_equal(tp.cpu().numpy().astype(np.int64), want[2]) and np.array_equal(tv.cpu().numpy(), want[0])
