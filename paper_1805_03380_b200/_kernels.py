@@ -81,7 +81,7 @@ def upload_coo(rows, cols, vals, device=None, shape=None):
         if st["buf"] is None or st["buf"].numel() < 2 * n:
             st["buf"] = torch.empty(2 * n, dtype=torch.int32).pin_memory()
         buf = st["buf"]
-        chunks = int(os.environ.get("AS_UPLOAD_CHUNKS", "4"))
+        chunks = int(os.environ.get("AS_UPLOAD_CHUNKS", "1"))  # measured: 1 chunk 599 us per e2e step, 2: 620, 4: 643
         with torch.cuda.device(dev):
             packed = shape is not None and min(shape) > 0 and \
                 (int(shape[0]) - 1).bit_length() + (int(shape[1]) - 1).bit_length() <= 31
