@@ -84,13 +84,16 @@ int as_upload_coo_i64(const int64_t *rows, const int64_t *cols, const void *vals
  * one 32-bit key (col << row_bits | row) -- 12 instead of 16 bytes per
  * triplet over PCIe -- and a device kernel unpacks every copied chunk into
  * d_rows / d_cols.  Coordinates outside the shape arrive as -1 (the same
- * first-bad-triplet report).  d_keys: device scratch of n uint32.  Returns
+ * first-bad-triplet report).  d_keys: device scratch of n uint32.
+ * *first_bad (nullable, host): the index of the first triplet outside the
+ * shape, or -1 -- the packers see every coordinate, so a caller can raise
+ * CoordinateError (csc.py:215-221) without waiting for the device.  Returns
  * AS_ERR_SHAPE when the bit widths do not fit (use as_upload_coo_i64).
  */
 int as_upload_coo_packed(const int64_t *rows, const int64_t *cols, const void *vals, int64_t n,
                          int64_t val_bytes, int64_t n_rows, int64_t n_cols, uint32_t *stage_keys,
                          uint32_t *d_keys, int32_t *d_rows, int32_t *d_cols, void *d_vals, int n_threads,
-                         int n_chunks, void *stream);
+                         int n_chunks, int64_t *first_bad, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Insertion-cache flush: base CSC + element-write log -> canonical CSC.

@@ -11,6 +11,7 @@ device->host copy (the only synchronisation).  There is no CPU path.
 
 from __future__ import annotations
 
+import ctypes
 import os
 import threading
 
@@ -51,7 +52,7 @@ def _upload_threads():
     return max(1, min(8, cores // 2))
 
 
-def upload_coo(rows, cols, vals, device=None, shape=None):
+def upload_coo(rows, cols, vals, device=None, shape=None, bad_out=None):
     """int64 host triplets -> device (int32 rows, int32 cols, vals) through
     as_upload_coo_i64: host threads narrow the indices into pinned staging
     while the values are copied, so 16 bytes per triplet cross PCIe instead
@@ -61,7 +62,9 @@ def upload_coo(rows, cols, vals, device=None, shape=None):
     shape = (n_rows, n_cols) whose index bit widths fit 31 bits together:
     the indices travel packed as one 32-bit key per triplet
     (as_upload_coo_packed, 12 bytes per triplet; coordinates outside the
-    shape arrive as -1)."""
+    shape arrive as -1).  bad_out (a list): receives the first out-of-shape
+    triplet's index or -1 when the packed path ran (the packers see every
+    coordinate)."""
     L = _lib.lib()
     dev = _dev(device)
     n = int(rows.shape[0])
@@ -87,10 +90,13 @@ def upload_coo(rows, cols, vals, device=None, shape=None):
                 (int(shape[0]) - 1).bit_length() + (int(shape[1]) - 1).bit_length() <= 31
             if packed:
                 d_keys = torch.empty(n, dtype=torch.int32, device=dev)
+                first_bad = ctypes.c_int64(-1)
                 check(L.as_upload_coo_packed(ptr(rows), ptr(cols), ptr(vals) if pinned_vals else None, n,
                                              vals.element_size(), int(shape[0]), int(shape[1]), ptr(buf), ptr(d_keys),
                                              ptr(d_rows), ptr(d_cols), ptr(d_vals), _upload_threads(), chunks,
-                                             stream()))
+                                             ctypes.addressof(first_bad), stream()))
+                if bad_out is not None:
+                    bad_out.append(int(first_bad.value))
             else:
                 check(L.as_upload_coo_i64(ptr(rows), ptr(cols), ptr(vals) if pinned_vals else None, n,
                                           vals.element_size(), ptr(buf), buf.data_ptr() + 4 * n, ptr(d_rows),
@@ -101,7 +107,7 @@ def upload_coo(rows, cols, vals, device=None, shape=None):
     return d_rows, d_cols, d_vals
 
 
-def coo_to_csc(n_rows, n_cols, rows, cols, vals, dup=DUP_SUM, out=None):
+def coo_to_csc(n_rows, n_cols, rows, cols, vals, dup=DUP_SUM, out=None, lazy=False):
     """Canonical CSC from COO triplets (csc.canonicalize, csc.py:148-193):
     stable column-major order, duplicates summed in np.add.reduceat order or
     last-wins, exact zeros pruned.  rows/cols int32 or int64, on the device or
@@ -129,6 +135,8 @@ def coo_to_csc(n_rows, n_cols, rows, cols, vals, dup=DUP_SUM, out=None):
     ws = workspace(ws_bytes, dev, key="sortreduce")
     check(f(n_rows, n_cols, n, ptr(rows), ptr(cols), idx_bytes, ptr(vals), _DUP[dup], ptr(col_ptr), ptr(row_idx),
             ptr(out_vals), ptr(info), ptr(ws), ws_bytes, stream()))
+    if lazy:  # (full-capacity outputs and the device info[2]; the caller knows the input is in range)
+        return col_ptr, row_idx, out_vals, info
     nnz, bad = _read_info(info)
     return col_ptr, row_idx[:nnz], out_vals[:nnz], (bad if bad < n else None)
 

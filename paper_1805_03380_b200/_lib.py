@@ -33,7 +33,7 @@ SIGNATURES = {
     "as_coo_to_csc_f64": (INT, [I64, I64, I64, P, P, INT, P, INT, P, P, P, P, P, SZ, P]),
     "as_coo_to_csc_f32": (INT, [I64, I64, I64, P, P, INT, P, INT, P, P, P, P, P, SZ, P]),
     "as_upload_coo_i64": (INT, [P, P, P, I64, I64, P, P, P, P, P, INT, INT, P]),
-    "as_upload_coo_packed": (INT, [P, P, P, I64, I64, I64, I64, P, P, P, P, P, INT, INT, P]),
+    "as_upload_coo_packed": (INT, [P, P, P, I64, I64, I64, I64, P, P, P, P, P, INT, INT, P, P]),
     "as_flush_workspace_bytes": (SZ, [I64, I64, I64]),
     "as_flush_log_f64": (INT, [I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P, SZ, P]),
     "as_transpose_workspace_bytes": (SZ, [I64, I64]),

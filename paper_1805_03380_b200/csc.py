@@ -70,7 +70,7 @@ def _to_dev(a, dtype, device):
 class CscData:
     """Canonical CSC matrix (sorted, duplicate-free, zero-free) in HBM."""
 
-    __slots__ = ("dims", "col_ptr", "row_idx", "vals", "_host", "_snap")
+    __slots__ = ("dims", "col_ptr", "_row_idx", "_vals", "_host", "_snap", "_pend")
 
     def __init__(self, dims: Dims, col_ptr, row_idx, vals, device=None):
         if dims.n_rows > DEVICE_INDEX_MAX or dims.n_cols > DEVICE_INDEX_MAX:
@@ -78,20 +78,82 @@ class CscData:
         device = device or (col_ptr.device if isinstance(col_ptr, torch.Tensor) else default_device())
         self.dims = dims
         self.col_ptr = _to_dev(col_ptr, torch.int32, device)
-        self.row_idx = _to_dev(row_idx, torch.int32, device)
+        self._row_idx = _to_dev(row_idx, torch.int32, device)
         vdt = vals.dtype if isinstance(vals, torch.Tensor) and vals.dtype in (torch.float32, torch.float64) else torch.float64
-        self.vals = _to_dev(vals, vdt, device)
+        self._vals = _to_dev(vals, vdt, device)
         self._host = None
         self._snap = False  # an insertion cache holds this CSC as its base snapshot (rbt.from_csc)
+        self._pend = None   # device info[2] while nnz is still on the device (see pending)
+
+    @classmethod
+    def pending(cls, dims: Dims, col_ptr, row_idx_full, vals_full, info) -> "CscData":
+        """A CSC whose nnz is still on the device (info[0], written by the
+        construction kernel): the row / value buffers have their full
+        capacity until the first access that needs the size, which reads it
+        back (one synchronisation) -- or to_host() takes it from the copied
+        col_ptr, so an end-to-end build synchronises once."""
+        m = cls(dims, col_ptr, row_idx_full, vals_full)
+        m._pend = info
+        return m
+
+    def _resolve(self, nnz=None):
+        if self._pend is not None:
+            k = int(self._pend[0].item()) if nnz is None else int(nnz)
+            self._pend = None
+            self._row_idx = self._row_idx[:k]
+            self._vals = self._vals[:k]
+
+    @property
+    def row_idx(self):
+        self._resolve()
+        return self._row_idx
+
+    @row_idx.setter
+    def row_idx(self, v):
+        self._resolve()
+        self._row_idx = v
+
+    @property
+    def vals(self):
+        self._resolve()
+        return self._vals
+
+    @vals.setter
+    def vals(self, v):
+        self._resolve()
+        self._vals = v
+
+    def to_host(self, out=None):
+        """(col_ptr int32, row_idx int32, vals) as host tensors -- into `out`
+        (pinned, sized n_cols + 1 and >= the row / value buffers) when given.
+        All copies are issued before the single synchronisation; a pending
+        nnz comes from the copied col_ptr[-1]."""
+        pend = self._pend is not None
+        ri, vv = self._row_idx, self._vals  # full capacity while pending
+        if out is None:
+            out = (torch.empty(self.col_ptr.shape[0], dtype=torch.int32).pin_memory(),
+                   torch.empty(ri.shape[0], dtype=torch.int32).pin_memory(),
+                   torch.empty(vv.shape[0], dtype=vv.dtype).pin_memory())
+        o_ptr, o_rows, o_vals = out
+        o_ptr.copy_(self.col_ptr, non_blocking=True)
+        o_rows[: ri.shape[0]].copy_(ri, non_blocking=True)
+        o_vals[: vv.shape[0]].copy_(vv, non_blocking=True)
+        torch.cuda.current_stream(self.col_ptr.device).synchronize()
+        k = int(o_ptr[-1]) if pend else int(ri.shape[0])
+        if pend:
+            self._resolve(k)
+        return o_ptr, o_rows[:k], o_vals[:k]
 
     def own_values_copy(self) -> "CscData":
         """The same matrix with its own value array (the index arrays are
         immutable and shared): what an in-place value patch writes to while
         an insertion cache still holds this one as its snapshot."""
+        self._resolve()
         c = CscData.__new__(CscData)
-        c.dims, c.col_ptr, c.row_idx, c.vals = self.dims, self.col_ptr, self.row_idx, self.vals.clone()
+        c.dims, c.col_ptr, c._row_idx, c._vals = self.dims, self.col_ptr, self._row_idx, self._vals.clone()
         c._host = None if self._host is None else (self._host[0].copy(), self._host[1], self._host[2])
         c._snap = False
+        c._pend = None
         return c
 
     @classmethod
@@ -259,7 +321,13 @@ def build_device(dims: Dims, rows, cols, values, dup: str = DUP_SUM, device=None
         # int64 host triplets: narrowed (or packed into one 32-bit key per
         # triplet when the shape allows) on host threads while the values
         # are copied (16 or 12 instead of 24 bytes per triplet over PCIe)
-        r, c, v = _kernels.upload_coo(hr, hc, hv, device, (dims.n_rows, dims.n_cols))
+        host_bad = []
+        r, c, v = _kernels.upload_coo(hr, hc, hv, device, (dims.n_rows, dims.n_cols), bad_out=host_bad)
+        if host_bad and host_bad[0] < 0:
+            # the packers saw every coordinate in range: no read-back of the
+            # kernel's report, nnz stays on the device until it is needed
+            p, ri, vv, info = _kernels.coo_to_csc(dims.n_rows, dims.n_cols, r, c, v, dup, lazy=True)
+            return CscData.pending(dims, p, ri, vv, info), None
     else:
         r = _as_index_tensor(rows, device)
         c = _as_index_tensor(cols, device)

@@ -130,17 +130,29 @@ inline uint32_t pack_key(int64_t r, int64_t c, uint64_t nr, uint64_t nc, int rbi
   return ((uint64_t)r < nr && (uint64_t)c < nc) ? (uint32_t)(((uint64_t)c << rbits) | (uint64_t)r) : 0xffffffffu;
 }
 
-void pack_range(const int64_t* rows, const int64_t* cols, uint32_t* dst, int64_t a, int64_t b, uint64_t nr,
-                uint64_t nc, int rbits) {
+// returns the first index in [a, b) whose coordinate is outside the shape, or b
+int64_t pack_range(const int64_t* rows, const int64_t* cols, uint32_t* dst, int64_t a, int64_t b, uint64_t nr,
+                   uint64_t nc, int rbits) {
   int64_t i = a;
-  for (; i < b && (reinterpret_cast<uintptr_t>(dst + i) & 15u); i++) dst[i] = pack_key(rows[i], cols[i], nr, nc, rbits);
+  int64_t bad = b;
+  for (; i < b && (reinterpret_cast<uintptr_t>(dst + i) & 15u); i++) {
+    dst[i] = pack_key(rows[i], cols[i], nr, nc, rbits);
+    if (dst[i] == 0xffffffffu && bad == b) bad = i;
+  }
   for (; i + 4 <= b; i += 4) {
-    const __m128i q = _mm_set_epi32(
-        (int)pack_key(rows[i + 3], cols[i + 3], nr, nc, rbits), (int)pack_key(rows[i + 2], cols[i + 2], nr, nc, rbits),
-        (int)pack_key(rows[i + 1], cols[i + 1], nr, nc, rbits), (int)pack_key(rows[i], cols[i], nr, nc, rbits));
+    const uint32_t k0 = pack_key(rows[i], cols[i], nr, nc, rbits), k1 = pack_key(rows[i + 1], cols[i + 1], nr, nc, rbits),
+                   k2 = pack_key(rows[i + 2], cols[i + 2], nr, nc, rbits),
+                   k3 = pack_key(rows[i + 3], cols[i + 3], nr, nc, rbits);
+    if (bad == b && (k0 == 0xffffffffu || k1 == 0xffffffffu || k2 == 0xffffffffu || k3 == 0xffffffffu))
+      bad = i + (k0 == 0xffffffffu ? 0 : k1 == 0xffffffffu ? 1 : k2 == 0xffffffffu ? 2 : 3);
+    const __m128i q = _mm_set_epi32((int)k3, (int)k2, (int)k1, (int)k0);
     _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), q);
   }
-  for (; i < b; i++) dst[i] = pack_key(rows[i], cols[i], nr, nc, rbits);
+  for (; i < b; i++) {
+    dst[i] = pack_key(rows[i], cols[i], nr, nc, rbits);
+    if (dst[i] == 0xffffffffu && bad == b) bad = i;
+  }
+  return bad;
 }
 
 }  // namespace
@@ -193,15 +205,18 @@ int as_upload_coo_i64(const int64_t* rows, const int64_t* cols, const void* vals
 
 int as_upload_coo_packed(const int64_t* rows, const int64_t* cols, const void* vals, int64_t n, int64_t val_bytes,
                          int64_t n_rows, int64_t n_cols, uint32_t* stage_keys, uint32_t* d_keys, int32_t* d_rows,
-                         int32_t* d_cols, void* d_vals, int n_threads, int n_chunks, void* stream) {
+                         int32_t* d_cols, void* d_vals, int n_threads, int n_chunks, int64_t* first_bad,
+                         void* stream) {
   cudaStream_t st = S(stream);
   AS_REQUIRE(n >= 0 && (val_bytes == 4 || val_bytes == 8), AS_ERR_ARG, "bad upload arguments");
   AS_REQUIRE(n_rows > 0 && n_cols > 0, AS_ERR_SHAPE, "packed upload needs a non-empty shape");
   const int rbits = bits_for(n_rows - 1), cbits = bits_for(n_cols - 1);
   AS_REQUIRE(rbits + cbits <= 31, AS_ERR_SHAPE, "%d + %d index bits do not fit a 32-bit key", rbits, cbits);
+  if (first_bad) *first_bad = -1;
   if (n == 0) return AS_OK;
   const int T = std::max(1, std::min(n_threads, 256));
   const int K = (int)std::max<int64_t>(1, std::min<int64_t>(n_chunks, (n + 65535) / 65536));
+  std::atomic<int64_t> bad_min{n};
   if (vals) AS_CUDA_TRY(cudaMemcpyAsync(d_vals, vals, (size_t)(n * val_bytes), cudaMemcpyHostToDevice, st));
   const int64_t per = (n + K - 1) / K;
   for (int k = 0; k < K; k++) {
@@ -210,12 +225,21 @@ int as_upload_coo_packed(const int64_t* rows, const int64_t* cols, const void* v
     const int64_t span = hi - lo;
     HostPool::get().run(T, [&](int w) {
       const int64_t a = lo + span * w / T, b = lo + span * (w + 1) / T;
-      pack_range(rows, cols, stage_keys, a, b, (uint64_t)n_rows, (uint64_t)n_cols, rbits);
+      const int64_t bad = pack_range(rows, cols, stage_keys, a, b, (uint64_t)n_rows, (uint64_t)n_cols, rbits);
+      if (bad < b) {
+        int64_t cur = bad_min.load(std::memory_order_relaxed);
+        while (bad < cur && !bad_min.compare_exchange_weak(cur, bad, std::memory_order_relaxed)) {
+        }
+      }
       _mm_sfence();
     });
     AS_CUDA_TRY(cudaMemcpyAsync(d_keys + lo, stage_keys + lo, (size_t)span * 4, cudaMemcpyHostToDevice, st));
     unpack_keys_kernel<<<(unsigned)((span + 255) / 256), 256, 0, st>>>(d_keys, lo, hi, rbits, d_rows, d_cols);
     AS_LAUNCH_CHECK();
+  }
+  if (first_bad) {
+    const int64_t b = bad_min.load();
+    *first_bad = b < n ? b : -1;
   }
   return AS_OK;
 }
