@@ -397,14 +397,18 @@ def main_device(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         sp_total = float(t[0])
     packed = (n_rows - 1).bit_length() + (n_cols - 1).bit_length() <= 31  # one 32-bit key per triplet
+    cap = n if packed else k
+    row_bytes = 2 if (n_rows <= 65536 and cap >= (1 << 16)) else 4
     e2e = {"value": e2e_value, "unit": "nnz/s", "h2d_bytes_per_step": (12 if packed else 16) * n,  # indices + f64
            # the row / value buffers travel at their full capacity (n): nnz is
            # not known on the host before the copies are issued
-           "d2h_bytes_per_step": 4 * (n_cols + 1) + (12 * n if packed else 12 * k),
+           # (rows of a matrix with <= 65536 rows travel as uint16)
+           "d2h_bytes_per_step": 4 * (n_cols + 1) + (row_bytes + 8) * cap,
            "ms_median": 1e3 * statistics.median(e2e_times), "ms_min": 1e3 * min(e2e_times),
            "ms_max": 1e3 * max(e2e_times),
            "path": "SpMat.from_triplets((rows i64, cols i64, vals f64) pinned host) -> .csc().to_host(pinned buffers), "
-                   "one synchronisation per step; "
+                   "one synchronisation per step; rows read back as uint16 (n_rows <= 65536) and widened on host threads "
+                   "while the values copy; "
                    + ("indices packed into one 32-bit key per triplet (col << 14 | row) on host threads while the "
                       "values are copied, unpacked by a device kernel (as_upload_coo_packed)" if packed else
                       "indices narrowed to int32 on host threads while the values are copied (as_upload_coo_i64)"),

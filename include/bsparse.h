@@ -95,6 +95,13 @@ int as_upload_coo_packed(const int64_t *rows, const int64_t *cols, const void *v
                          uint32_t *d_keys, int32_t *d_rows, int32_t *d_cols, void *d_vals, int n_threads,
                          int n_chunks, int64_t *first_bad, void *stream);
 
+/* Read-back of a CSC's row indices at half width (host side of
+ * CscData.to_host when every row is < 65536): d_rows -> uint16 on the device
+ * (d_scratch, n uint16) -> pinned h_stage, asynchronous on `stream`; then
+ * as_widen_u16 (host threads) once the copy has landed. */
+int as_rows_to_host_u16(const int32_t *d_rows, int64_t n, uint16_t *d_scratch, uint16_t *h_stage, void *stream);
+int as_widen_u16(const uint16_t *src, int32_t *dst, int64_t n, int n_threads);
+
 /* ---------------------------------------------------------------------------
  * Insertion-cache flush: base CSC + element-write log -> canonical CSC.
  * Replaces rbt.to_csc (rbt.py:444-458) of the tree that RbtStore.insert

@@ -107,6 +107,22 @@ def upload_coo(rows, cols, vals, device=None, shape=None, bad_out=None):
     return d_rows, d_cols, d_vals
 
 
+_u16 = {}
+
+
+def u16_stage(n, device):
+    """Pinned uint16 host stage and device scratch for CscData.to_host's
+    half-width row read-back (kept per device, grown on demand).  One
+    read-back at a time per device (the stage is waited on before reuse)."""
+    key = torch.device(device).index
+    st = _u16.get(key)
+    if st is None or st[0].numel() < n:
+        st = (torch.empty(max(n, 1), dtype=torch.int16).pin_memory(),
+              torch.empty(max(n, 1), dtype=torch.int16, device=device))
+        _u16[key] = st
+    return st
+
+
 def coo_to_csc(n_rows, n_cols, rows, cols, vals, dup=DUP_SUM, out=None, lazy=False):
     """Canonical CSC from COO triplets (csc.canonicalize, csc.py:148-193):
     stable column-major order, duplicates summed in np.add.reduceat order or

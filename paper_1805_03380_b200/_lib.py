@@ -34,6 +34,8 @@ SIGNATURES = {
     "as_coo_to_csc_f32": (INT, [I64, I64, I64, P, P, INT, P, INT, P, P, P, P, P, SZ, P]),
     "as_upload_coo_i64": (INT, [P, P, P, I64, I64, P, P, P, P, P, INT, INT, P]),
     "as_upload_coo_packed": (INT, [P, P, P, I64, I64, I64, I64, P, P, P, P, P, INT, INT, P, P]),
+    "as_rows_to_host_u16": (INT, [P, I64, P, P, P]),
+    "as_widen_u16": (INT, [P, P, I64, INT]),
     "as_flush_workspace_bytes": (SZ, [I64, I64, I64]),
     "as_flush_log_f64": (INT, [I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P, SZ, P]),
     "as_transpose_workspace_bytes": (SZ, [I64, I64]),

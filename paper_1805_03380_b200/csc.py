@@ -17,6 +17,8 @@ from typing import Iterator, NamedTuple, Sequence
 import numpy as np
 import torch
 
+from . import _lib
+
 from . import _kernels
 from .errors import CoordinateError, CorruptionError
 
@@ -128,6 +130,12 @@ class CscData:
         (pinned, sized n_cols + 1 and >= the row / value buffers) when given.
         All copies are issued before the single synchronisation; a pending
         nnz comes from the copied col_ptr[-1]."""
+        if self.col_ptr.device.type == "cpu":  # a host CSC (canonicalize_host)
+            if out is None:
+                return self.col_ptr, self.row_idx, self.vals
+            k = self.nnz
+            out[0].copy_(self.col_ptr), out[1][:k].copy_(self.row_idx), out[2][:k].copy_(self.vals)
+            return out[0], out[1][:k], out[2][:k]
         pend = self._pend is not None
         ri, vv = self._row_idx, self._vals  # full capacity while pending
         if out is None:
@@ -135,11 +143,28 @@ class CscData:
                    torch.empty(ri.shape[0], dtype=torch.int32).pin_memory(),
                    torch.empty(vv.shape[0], dtype=vv.dtype).pin_memory())
         o_ptr, o_rows, o_vals = out
+        stream = torch.cuda.current_stream(self.col_ptr.device)
         o_ptr.copy_(self.col_ptr, non_blocking=True)
-        o_rows[: ri.shape[0]].copy_(ri, non_blocking=True)
+        n_r = int(ri.shape[0])
+        half = self.dims.n_rows <= 65536 and n_r >= (1 << 16)
+        if half:
+            # rows < 65536: they travel at half width and are widened on host
+            # threads while the values are still being copied
+            from . import _kernels
+
+            stage, scratch = _kernels.u16_stage(n_r, self.col_ptr.device)
+            _lib.check(_lib.lib().as_rows_to_host_u16(_lib.ptr(ri), n_r, _lib.ptr(scratch), _lib.ptr(stage),
+                                                      stream.cuda_stream))
+            rows_done = torch.cuda.Event()
+            rows_done.record(stream)
+        else:
+            o_rows[:n_r].copy_(ri, non_blocking=True)
         o_vals[: vv.shape[0]].copy_(vv, non_blocking=True)
-        torch.cuda.current_stream(self.col_ptr.device).synchronize()
-        k = int(o_ptr[-1]) if pend else int(ri.shape[0])
+        if half:
+            rows_done.synchronize()
+            _lib.check(_lib.lib().as_widen_u16(_lib.ptr(stage), _lib.ptr(o_rows), n_r, _kernels._upload_threads()))
+        stream.synchronize()
+        k = int(o_ptr[-1]) if pend else n_r
         if pend:
             self._resolve(k)
         return o_ptr, o_rows[:k], o_vals[:k]
@@ -178,11 +203,8 @@ class CscData:
     # -- reference-typed host mirror (csc.py:54-67) -----------------------------
     def _mirror(self):
         if self._host is None:
-            self._host = (
-                self.vals.double().cpu().numpy(),
-                self.row_idx.cpu().numpy().astype(np.int64),
-                self.col_ptr.cpu().numpy().astype(np.int64),
-            )
+            p, r, v = self.to_host()
+            self._host = (v.numpy().astype(np.float64), r.numpy().astype(np.int64), p.numpy().astype(np.int64))
         return self._host
 
     @property

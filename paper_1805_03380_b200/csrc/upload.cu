@@ -169,6 +169,13 @@ __global__ void __launch_bounds__(256) unpack_keys_kernel(const uint32_t* __rest
   cols[i] = bad ? -1 : (int32_t)(k >> rbits);
 }
 
+// row indices < 65536 -> uint16 (the CSC's rows travel back at half width)
+__global__ void __launch_bounds__(256) narrow_u16_kernel(const int32_t* __restrict__ src, long long n,
+                                                         uint16_t* __restrict__ dst) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = (uint16_t)__ldcs(&src[i]);
+}
+
 }  // namespace as
 
 using namespace as;
@@ -241,6 +248,31 @@ int as_upload_coo_packed(const int64_t* rows, const int64_t* cols, const void* v
     const int64_t b = bad_min.load();
     *first_bad = b < n ? b : -1;
   }
+  return AS_OK;
+}
+
+// D2H of row indices at half width: d_rows (all < 65536) -> uint16 on the
+// device, copied into the pinned stage; the caller widens after the copy
+// (as_widen_u16) while other copies are in flight.
+int as_rows_to_host_u16(const int32_t* d_rows, int64_t n, uint16_t* d_scratch, uint16_t* h_stage, void* stream) {
+  cudaStream_t st = S(stream);
+  AS_REQUIRE(n >= 0, AS_ERR_ARG, "negative length");
+  if (n == 0) return AS_OK;
+  narrow_u16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_rows, n, d_scratch);
+  AS_LAUNCH_CHECK();
+  AS_CUDA_TRY(cudaMemcpyAsync(h_stage, d_scratch, (size_t)n * 2, cudaMemcpyDeviceToHost, st));
+  return AS_OK;
+}
+
+// dst[i] = src[i] on host threads (the pinned uint16 stage -> int32 rows)
+int as_widen_u16(const uint16_t* src, int32_t* dst, int64_t n, int n_threads) {
+  AS_REQUIRE(n >= 0, AS_ERR_ARG, "negative length");
+  if (n == 0) return AS_OK;
+  const int T = std::max(1, std::min(n_threads, 256));
+  HostPool::get().run(T, [&](int w) {
+    const int64_t a = n * w / T, b = n * (w + 1) / T;
+    for (int64_t i = a; i < b; i++) dst[i] = (int32_t)src[i];
+  });
   return AS_OK;
 }
 

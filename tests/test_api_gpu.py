@@ -400,3 +400,26 @@ def test_rbt_snapshot_not_aliased_by_in_place_patch():
     assert m.get(2, 1) == 7.5
     assert t.get(encode_index(2, 1, 4)) == 3.0
     assert m.csc().values.tolist() == [1.0, 7.5, 2.0]
+
+
+@pytest.mark.parametrize("nr,nc,n", [(10000, 10000, 300000), (65536, 8, 70000), (65537, 8, 70000),
+                                     (300, 2, 5000), (1 << 20, 3, 100000)])
+def test_to_host_read_back(nr, nc, n):
+    """CscData.to_host (the e2e read-back): rows of a matrix with <= 65536 rows
+    come back at half width and are widened on host threads; the copied
+    col_ptr / rows / values equal the device arrays, also from a pending
+    (lazily sized) build and into caller-provided pinned buffers."""
+    rng = np.random.default_rng(nr + n)
+    rows, cols, vals = rng.integers(0, nr, n), rng.integers(0, nc, n), rng.uniform(-1, 1, n)
+    rows[0], cols[0] = nr - 1, nc - 1
+    want = oracle.canonicalize(nr, nc, rows, cols, vals)
+    for out in (None, "pinned"):
+        h = tuple(torch.from_numpy(x).pin_memory() for x in (rows, cols, vals))
+        data = SpMat.from_triplets(nr, nc, h).csc()
+        if out == "pinned":
+            out = (torch.empty(nc + 1, dtype=torch.int32).pin_memory(), torch.empty(n, dtype=torch.int32).pin_memory(),
+                   torch.empty(n, dtype=torch.float64).pin_memory())
+        p, r, v = data.to_host(out=out)
+        assert np.array_equal(p.numpy(), want[2]) and np.array_equal(r.numpy(), want[1])
+        assert np.array_equal(v.numpy().view(np.int64), want[0].view(np.int64))
+        assert torch.equal(data.row_idx.cpu(), r) and data.nnz == r.shape[0]
