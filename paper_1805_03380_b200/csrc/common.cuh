@@ -332,6 +332,40 @@ struct GridBar {
 };
 
 // Sense-free grid barrier for a cooperatively launched (co-resident) grid.
+// ------------------------------------------------------------------------
+// Bulk asynchronous copies (the TMA engine's 1-D mode) into shared memory,
+// completed on a shared-memory mbarrier: one elected thread moves a whole
+// contiguous range, no per-thread copy instructions.  Both addresses 16-byte
+// aligned and the size a multiple of 16 (callers guarantee it).
+AS_DEVICE_INLINE void mbar_init(unsigned long long* bar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// the calling thread arrives and announces `bytes` of transfers, then issues
+// the copy of `bytes` from gsrc to sdst
+AS_DEVICE_INLINE void bulk_g2s(void* sdst, const void* gsrc, unsigned bytes, unsigned long long* bar) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+               "l"(gsrc), "r"(bytes), "r"(b)
+               : "memory");
+}
+
+AS_DEVICE_INLINE void mbar_wait(unsigned long long* bar, unsigned parity) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(b), "r"(parity)
+        : "memory");
+  }
+}
+
 AS_DEVICE_INLINE unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

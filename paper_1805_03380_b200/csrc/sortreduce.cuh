@@ -58,6 +58,18 @@ namespace sr {
 constexpr int kThreads = AS_SR_THREADS;
 constexpr int kMinBlocks = AS_SR_MINB;         // co-resident CTAs per SM
 constexpr int kPer = 8;                        // P1: elements per thread (two groups of 4)
+// P1 values by bulk copies (cp.async.bulk on an mbarrier, UBLKCP / SYNCS in
+// the SASS) instead of per-thread cp.async: measured no faster (ncu build
+// 47.0 vs 47.2 us, transpose 46.8 vs 45.6 us; event time +1-2 us with 1, 4, 8
+// or 16 copies per CTA), so off by default -- a build knob
+#ifndef AS_SR_BULK
+#define AS_SR_BULK 0
+#endif
+constexpr bool kBulkVals = AS_SR_BULK != 0;
+#ifndef AS_SR_BULK_PARTS
+#define AS_SR_BULK_PARTS 4
+#endif
+constexpr int kBulkParts = AS_SR_BULK_PARTS;
 constexpr int kChunkMax = kThreads * kPer;     // elements per CTA chunk
 constexpr int kTile = AS_SR_TILE;              // elements of a shared-memory tile
 constexpr int kTP = kTile / kThreads;          // tile elements per thread
@@ -474,11 +486,12 @@ AS_DEVICE_INLINE void cp_async_vals4(T* sdst, const T* gsrc, long long i, long l
 
 template <class IdxT, class T>
 __device__ __forceinline__ unsigned ld_group(const Coo<IdxT, T>& s, const CscCtx&, const int*, long long e0,
-                                             long long hi, unsigned* mj, unsigned* mn, T* vdst, long long* bad) {
+                                             long long hi, unsigned* mj, unsigned* mn, T* vdst, long long* bad,
+                                             bool vbulk = false) {
   long long r[4], c[4];
   ld4_idx(s.rows, e0, hi, r);
   ld4_idx(s.cols, e0, hi, c);
-  cp_async_vals4(vdst, s.vals + e0, 0, hi - e0);
+  if (!vbulk) cp_async_vals4(vdst, s.vals + e0, 0, hi - e0);
   unsigned ok = 0;
 #pragma unroll
   for (int k = 0; k < 4; k++) {
@@ -496,10 +509,11 @@ __device__ __forceinline__ unsigned ld_group(const Coo<IdxT, T>& s, const CscCtx
 
 template <class T>
 __device__ __forceinline__ unsigned ld_group(const Csc<T>& s, const CscCtx& cx, const int* colc, long long e0,
-                                             long long hi, unsigned* mj, unsigned* mn, T* vdst, long long*) {
+                                             long long hi, unsigned* mj, unsigned* mn, T* vdst, long long*,
+                                             bool vbulk = false) {
   long long r[4];
   ld4_idx(s.idx, e0, hi, r);
-  cp_async_vals4(vdst, s.vals + e0, 0, hi - e0);
+  if (!vbulk) cp_async_vals4(vdst, s.vals + e0, 0, hi - e0);
   long long c;
   if (cx.cached) {
     int l = 0, h = (int)(cx.ce - cx.cb);
@@ -1113,6 +1127,29 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) sortreduce_kernel(Args<T
   const long long lo = min(a.n, g * ch), hi = min(a.n, lo + ch);
   const Layout LC = layout<T>(ncb, ch);
   T* st_val = reinterpret_cast<T*>(smem + LC.st_val);
+  // one source: the chunk's values travel to shared memory by bulk copies
+  // (TMA engine, kBulkParts pieces, completed on one mbarrier) issued before
+  // anything else; two sources (the flush) keep per-thread cp.async
+  __shared__ __align__(8) unsigned long long vbar;
+  const bool vbulk = !kTwoSrc && kBulkVals && hi > lo && ((reinterpret_cast<unsigned long long>(a.s1.vals) & 15ull) == 0);
+  if (vbulk && warp == 0) {
+    const long long body = ((hi - lo) * (long long)sizeof(T)) & ~15ll;  // bytes
+    const long long part = (((body + kBulkParts - 1) / kBulkParts) + 15) & ~15ll;
+    if (lane == 0) {
+      mbar_init(&vbar, kBulkParts);
+      for (long long e = lo + body / (long long)sizeof(T); e < hi; e++) st_val[e - lo] = __ldg(&a.s1.vals[e]);
+    }
+    __syncwarp();
+    if (lane < kBulkParts) {
+      const long long b0 = min(body, lane * part), b1 = min(body, b0 + part);
+      if (b1 > b0)
+        bulk_g2s(reinterpret_cast<unsigned char*>(st_val) + b0,
+                 reinterpret_cast<const unsigned char*>(a.s1.vals + lo) + b0, (unsigned)(b1 - b0), &vbar);
+      else
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(&vbar))
+                     : "memory");
+    }
+  }
   unsigned* st_key = reinterpret_cast<unsigned*>(smem + LC.st_key);
   unsigned short* st_idx = reinterpret_cast<unsigned short*>(smem + LC.st_idx);  // local input index
   for (long long t = tid; t <= ncb; t += kThreads) {
@@ -1150,7 +1187,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) sortreduce_kernel(Args<T
     unsigned o = 0;
     if (e0 < hi) {
       if (!kTwoSrc || e0 + 4 <= a.n1 || hi <= a.n1) {
-        o = ld_group(a.s1, cx1, colc, e0, min(hi, a.n1), mj + 4 * q, mn + 4 * q, vd, &bad);
+        o = ld_group(a.s1, cx1, colc, e0, min(hi, a.n1), mj + 4 * q, mn + 4 * q, vd, &bad, vbulk);
       } else if constexpr (kTwoSrc) {
         if (e0 >= a.n1) {
           long long b2 = a.n;
@@ -1234,6 +1271,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) sortreduce_kernel(Args<T
   SR_CLK(13, true);
   if (kDbg && a.stop == 13) return;
   asm volatile("cp.async.wait_all;" ::: "memory");
+  if (vbulk) mbar_wait(&vbar, 0);
   __syncthreads();
   {  // the chunk in bucket order, contiguous (coalesced): its bucket runs are
      // what the tiles gather
