@@ -182,6 +182,19 @@ int as_spmm_csr_f64(int64_t n_rows, int64_t n_cols, int64_t k, const int32_t *ro
                     const int32_t *col_idx, const double *vals, const double *B, int64_t ldb, double *C,
                     int64_t ldc, void *ws, size_t ws_bytes, void *stream);
 
+/* SpMM C = A @ B straight over the CSC of A (col_ptr[n_cols+1], row_idx,
+ * vals; nnz entries), no CSR: the column-merge variant, in the reference's
+ * own loop order (_kernels.mat_times_vec, _kernels.py:118-127: for each
+ * column, y[row] += val * x[col]).  Float32, additions in arrival order
+ * (tolerance 1e-5; not bit-reproducible run to run).  Used for the first
+ * product on a fresh CSC, when no CSR is cached (ops.mat_times_vec,
+ * ops.py:97-107).  ws: as_spmm_csc_workspace_bytes (a row-major n_rows x 16
+ * float32 accumulator and the tile table). */
+size_t as_spmm_csc_workspace_bytes(int64_t n_rows, int64_t nnz);
+int as_spmm_csc_f32(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t k, const int32_t *col_ptr,
+                    const int32_t *row_idx, const float *vals, const float *B, int64_t ldb, float *C,
+                    int64_t ldc, void *ws, size_t ws_bytes, void *stream);
+
 /* w = v^T A.  Replaces _kernels.vec_times_mat (_kernels.py:106-115). */
 int as_vecmat_csc_f64(int64_t n_rows, int64_t n_cols, const int32_t *col_ptr, const int32_t *row_idx,
                       const double *vals, const double *v, double *w, void *stream);

@@ -354,6 +354,20 @@ AS_DEVICE_INLINE void bulk_g2s(void* sdst, const void* gsrc, unsigned bytes, uns
                : "memory");
 }
 
+// one arrival announcing `bytes` of transfers (then issue the copies with
+// bulk_g2s_noarrive): lets one mbarrier of count 1 track several copies
+AS_DEVICE_INLINE void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+}
+AS_DEVICE_INLINE void bulk_g2s_noarrive(void* sdst, const void* gsrc, unsigned bytes, unsigned long long* bar) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+               "l"(gsrc), "r"(bytes), "r"(b)
+               : "memory");
+}
+
 AS_DEVICE_INLINE void mbar_wait(unsigned long long* bar, unsigned parity) {
   const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
   unsigned done = 0;

@@ -65,6 +65,9 @@ def test_cfg3_spmm_f32():
     assert np.all(np.abs(C - want) <= 1e-5 * np.maximum(1.0, np.abs(want)))
     Ce = _kernels.spmm(n, n, csr, Bd, exact=True).cpu().numpy().astype(np.float64)
     assert np.array_equal(Ce, want.astype(np.float32).astype(np.float64))
+    # column merge straight over the CSC (the first product on a fresh handle)
+    Cm = _kernels.spmm_csc(n, n, A, Bd).cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(Cm - want) <= 1e-5 * np.maximum(1.0, np.abs(want)))
 
 
 def test_cfg4_trace():
