@@ -348,7 +348,7 @@ spmm_csc_merge_kernel(long long n_cols, long long nnz, long long T, const int* _
                       int hints) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CmSmem& S = *reinterpret_cast<CmSmem*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int g = tid >> 2, s = tid & 3;
   const long long t = blockIdx.x;
   const long long e0 = t * kCmE, e1 = min(nnz, e0 + kCmE);

@@ -56,9 +56,10 @@ def _B(rng, n, k, ld=None, offset=0):
 
 
 @pytest.mark.parametrize("k", [1, 5, 16, 17, 64])
-def test_spmm_csc_uniform(K, k):
+@pytest.mark.parametrize("n_rows", [30000, 30003])  # (30003: C's columns unaligned, a partial row quad)
+def test_spmm_csc_uniform(K, k, n_rows):
     rng = np.random.default_rng(50 + k)
-    n_rows, n_cols, nnz = 30000, 20000, 200000
+    n_cols, nnz = 20000, 200000
     a = _case(rng, n_rows, n_cols, rng.integers(0, n_rows, nnz), rng.integers(0, n_cols, nnz))
     B, Bn = _B(rng, n_cols, k)
     want = oracle.spmm(*a, Bn, n_rows, n_cols, nthreads=8)
