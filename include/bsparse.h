@@ -212,6 +212,11 @@ int as_trace_atb_f64(int64_t n_rows, int64_t n_cols, const int32_t *a_col_ptr, c
                      const double *a_vals, const int32_t *b_col_ptr, const int32_t *b_row_idx,
                      const double *b_vals, int64_t nnz_a, int64_t nnz_b, double *out, void *ws,
                      size_t ws_bytes, void *stream);
+/* Trace kernel selection (tests and measurements only): 0 = automatic (the
+ * tile kernel: column-pair tiles staged by bulk copies, lanes merging list
+ * segments; falls back when the row arrays are not 16-byte aligned), 1 = the
+ * warp-per-column kernel.  Process-wide. */
+int as_set_trace_engine(int engine);
 
 /* ---------------------------------------------------------------------------
  * construction-funnelled ops and segmented reductions of the

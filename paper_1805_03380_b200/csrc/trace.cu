@@ -3,14 +3,17 @@
 // Replaces _kernels.fused_trace (_kernels.py:153-175): sum over columns j of
 // the products of coincident nonzeros of A[:,j] and B[:,j].
 //
-// B200 design: the (A,B) column pairs are laid end to end as one merged
-// sequence of length nnzA + nnzB; every thread owns kItems consecutive
-// positions of it (merge path), so the work is balanced whatever the column
-// lengths, every row index is read exactly once (coalesced per warp), and
-// values are gathered only at matches.  Partial sums are double-double
-// (TwoSum) and reduced in a fixed tree, so the result is deterministic and
-// within an ulp or two of the exactly rounded sum; the reference's sequential
-// left fold (_kernels.py:158-168) differs from it only by its own rounding.
+// B200 design: two kernels, picked on the host from the mean column length.
+// Up to 384 entries per column the warp-tile kernel runs (a warp's consecutive
+// column pairs staged in shared memory by bulk copies -- TMA -- in a per-warp
+// software pipeline, 2^LG lanes per pair merging list segments with two
+// cursors); beyond, or when the row arrays are not 16-byte aligned, the
+// warp-per-column kernel (register lists, a shared-memory row filter, deferred
+// searches).  Every row index is read once, values are gathered only at
+// matches.  Partial sums are double-double (TwoSum) and reduced in fixed
+// trees, so the result is deterministic and within an ulp or two of the
+// exactly rounded sum; the reference's sequential left fold
+// (_kernels.py:158-168) differs from it only by its own rounding.
 #include "capi_util.cuh"
 #include "common.cuh"
 #include "merge.cuh"
@@ -20,8 +23,6 @@
 namespace as {
 
 constexpr int kTrThreads = 256;
-constexpr int kTrItems = 32;
-constexpr int kTrChunk = kTrThreads * kTrItems;
 
 struct DD {
   double s, e;
@@ -247,6 +248,316 @@ trace_partial_kernel(long long n_cols, const int* __restrict__ ap, const int* __
   }
 }
 
+// ------------------------------------------------------------------------
+// Warp-tile kernel (the default for mean column lengths up to kTwMaxMean): a
+// warp takes 32 >> LG consecutive column pairs, 2^LG lanes per pair (LG picked
+// on the host from the mean column length, <= 13 entries of each list per
+// lane).  The pairs' row lists are contiguous in the CSC arrays, so a warp's
+// tile -- A's run and B's run -- comes into the warp's shared-memory buffers
+// with two bulk copies (the TMA engine's 1-D mode) completed on the warp's
+// mbarrier; no thread issues a load for a row index.  Every warp runs its own
+// three-stage software pipeline with no CTA barrier: the column pointers of
+// tile k + 2 are in flight (registers) and the bulk copies of tile k + 1 land
+// in the other buffer while tile k is merged.  A pair's lanes split the longer
+// list into equal segments; each lane finds where its segment starts in the
+// shorter list (one lower_bound in shared memory) and runs a branch-free
+// two-pointer merge of its segment against it on shared-memory byte addresses
+// (~17 instructions per list entry and lane; the warp-per-column kernel spends
+// ~430 warp instructions per column pair at cfg 4, this one ~190).  Pairs
+// far above the mean (more than kTwLongPerLane entries per lane) are searched
+// by the whole warp afterwards (every lane a stride of the shorter list, a
+// lower_bound in the longer one, both in shared memory); a tile whose runs
+// exceed the buffers is searched pair by pair in global memory.  Tiles are
+// assigned round-robin (static), every lane sums its matches in column order
+// in double-double, and the block / grid reductions are fixed trees:
+// deterministic.
+// Measured on cfg 4: a CTA-wide variant (256 threads, 64 pairs per tile, one
+// buffer, CTA barriers) ran 59 us -- every CTA of the grid loads, then every
+// CTA merges, in lockstep, so the memory system and the issue slots idle in
+// turn; the per-warp pipeline removes the lockstep.
+#ifndef AS_TW_WARPS
+#define AS_TW_WARPS 8      // 3 CTAs x 8 warps x 2 stages x 2 lists x 584 entries = 224 KB per SM
+#define AS_TW_CAP 576
+#define AS_TW_PER_LANE 13  // a warp tile holds <= 32 x 13 = 416 entries of each list at the mean: 72 % of a buffer
+#endif
+constexpr int kTwWarps = AS_TW_WARPS;  // warps per CTA
+constexpr int kTwThreads = kTwWarps * 32;
+constexpr int kTwCap = AS_TW_CAP;      // entries per list buffer of a warp
+constexpr int kTwStride = kTwCap + 8; // + alignment slack (a run starts up to 3 entries into its first quad)
+constexpr int kTwLongPerLane = 128;   // a pair with more entries per lane goes to the whole warp
+constexpr int kTwPerLane = AS_TW_PER_LANE;        // target entries of each list per lane (picks LG)
+constexpr int kTwMaxMean = 384;       // beyond: the warp-per-column kernel
+
+struct TwSmem {
+  alignas(16) int buf[kTwWarps][2][2][kTwStride];  // [warp][stage][A, B][entries]
+  alignas(8) unsigned long long bar[kTwWarps][2];
+  DD s_warp[kTwWarps];
+  int s_last;
+};
+
+AS_DEVICE_INLINE int tt_lower_bound(const int* __restrict__ s, int n, int key) {
+  int lo = 0;
+  while (n > 0) {
+    const int half = n >> 1;
+    const bool right = s[lo + half] < key;
+    lo = right ? lo + half + 1 : lo;
+    n = right ? n - half - 1 : half;
+  }
+  return lo;
+}
+
+AS_DEVICE_INLINE int tt_lds(unsigned addr) {
+  int v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// one merge step for l != s: the cursor of the smaller entry moves on.  Each
+// cursor keeps its next entry prefetched in a register (ln / sn), so the
+// compare of the following step never waits for a shared-memory load issued
+// in this one: the loop-carried chain is compare -> move, and the prefetch has
+// a whole step (two when the cursors alternate) to arrive.
+AS_DEVICE_INLINE void tt_step(unsigned& pl, unsigned& ps, int& l, int& s, int& ln, int& sn) {
+  asm volatile(
+      "{\n .reg .pred q1, q2;\n setp.lt.s32 q1, %2, %3;\n setp.lt.s32 q2, %3, %2;\n"
+      " @q1 mov.b32 %2, %4;\n @q2 mov.b32 %3, %5;\n"
+      " @q1 add.u32 %0, %0, 4;\n @q2 add.u32 %1, %1, 4;\n"
+      " @q1 ld.shared.b32 %4, [%0+4];\n @q2 ld.shared.b32 %5, [%1+4];\n}"
+      : "+r"(pl), "+r"(ps), "+r"(l), "+r"(s), "+r"(ln), "+r"(sn));
+}
+
+// every entry of the shorter list (a stride per lane) searched in the longer one
+template <bool kGlobal>
+AS_DEVICE_INLINE void tw_search_pair(DD& acc, int lane, const int* La, const int* Lb, int a0, int a1, int b0, int b1,
+                                     const double* __restrict__ av, const double* __restrict__ bv) {
+  // La / Lb point at the pair's first A / B entry (shared or global memory)
+  const int la = a1 - a0, lb = b1 - b0;
+  if (la == 0 || lb == 0) return;
+  const bool a_long = la >= lb;
+  const int* L = a_long ? La : Lb;
+  const int* Sh = a_long ? Lb : La;
+  const int ll = a_long ? la : lb, sl = a_long ? lb : la;
+  for (int q = lane; q < sl; q += 32) {
+    const int r = kGlobal ? __ldg(&Sh[q]) : Sh[q];
+    int lo = 0, n = ll;
+    while (n > 0) {
+      const int half = n >> 1;
+      const int v = kGlobal ? __ldg(&L[lo + half]) : L[lo + half];
+      const bool right = v < r;
+      lo = right ? lo + half + 1 : lo;
+      n = right ? n - half - 1 : half;
+    }
+    if (lo < ll && (kGlobal ? __ldg(&L[lo]) : L[lo]) == r)
+      dd_add_match(acc, av, bv, a_long ? a0 + lo : a0 + q, a_long ? b0 + q : b0 + lo);
+  }
+}
+
+template <int LG>
+__global__ void __launch_bounds__(kTwThreads, 3)
+trace_warp_tile_kernel(long long n_cols, const int* __restrict__ ap, const int* __restrict__ ar,
+                       const double* __restrict__ av, const int* __restrict__ bp, const int* __restrict__ br,
+                       const double* __restrict__ bv, int nnz_a, int nnz_b, DD* partials, unsigned* done,
+                       double* out) {
+  extern __shared__ __align__(16) unsigned char tw_raw[];
+  TwSmem& S = *reinterpret_cast<TwSmem*>(tw_raw);
+  constexpr int G = 1 << LG;   // lanes per column pair
+  constexpr int WC = 32 >> LG; // column pairs per warp tile
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int lc = lane >> LG, sub = lane & (G - 1);
+  const long long n_tiles = (n_cols + WC - 1) / WC;
+  const long long nW = (long long)gridDim.x * kTwWarps;
+  DD acc{0.0, 0.0};
+  if (lane == 0) {
+    mbar_init(&S.bar[wib][0], 1);
+    mbar_init(&S.bar[wib][1], 1);
+  }
+  __syncwarp();
+  // a tile's column pointers: lane q holds those of column c0 + q (clamped to
+  // n_cols, so columns past the end read as empty), plus the tile's last one
+  auto load_ptrs = [&](long long tile, int& pa, int& pb, int& pa_last, int& pb_last) {
+    pa = pb = pa_last = pb_last = 0;
+    if (tile < n_tiles) {
+      const long long c0 = tile * WC;
+      const long long c = c0 + lane < n_cols ? c0 + lane : n_cols;
+      pa = __ldg(&ap[c]);
+      pb = __ldg(&bp[c]);
+      if (WC == 32) {
+        const long long ce = c0 + WC < n_cols ? c0 + WC : n_cols;
+        pa_last = __ldg(&ap[ce]);
+        pb_last = __ldg(&bp[ce]);
+      }
+    }
+  };
+  // issue the tile's bulk copies into `stage`; false when its runs exceed the buffers
+  auto issue = [&](int stage, int pa, int pb, int pa_last, int pb_last) -> bool {
+    const int a_lo = __shfl_sync(0xffffffffu, pa, 0), b_lo = __shfl_sync(0xffffffffu, pb, 0);
+    const int a_hi = WC == 32 ? pa_last : __shfl_sync(0xffffffffu, pa, WC & 31);
+    const int b_hi = WC == 32 ? pb_last : __shfl_sync(0xffffffffu, pb, WC & 31);
+    const int a_base = a_lo & ~3, b_base = b_lo & ~3;
+    if (a_hi - a_base > kTwCap || b_hi - b_base > kTwCap) return false;
+    // the copies end at the next 16-byte boundary, or at the last one inside
+    // the array (then the array's last < 4 entries come by plain loads)
+    const int a_end = min((a_hi + 3) & ~3, nnz_a & ~3), b_end = min((b_hi + 3) & ~3, nnz_b & ~3);
+    int* sa = S.buf[wib][stage][0];
+    int* sb = S.buf[wib][stage][1];
+    if (lane == 0) {
+      const unsigned na = a_end > a_base ? (unsigned)(a_end - a_base) * 4u : 0u;
+      const unsigned nb = b_end > b_base ? (unsigned)(b_end - b_base) * 4u : 0u;
+      mbar_expect_tx(&S.bar[wib][stage], na + nb);
+      if (na) bulk_g2s_noarrive(sa, ar + a_base, na, &S.bar[wib][stage]);
+      if (nb) bulk_g2s_noarrive(sb, br + b_base, nb, &S.bar[wib][stage]);
+    }
+    if (a_hi > a_end && lane < 4) {
+      const int q = max(a_end, a_base) + lane;
+      if (q < a_hi) sa[q - a_base] = __ldg(&ar[q]);
+    }
+    if (b_hi > b_end && lane >= 4 && lane < 8) {
+      const int q = max(b_end, b_base) + lane - 4;
+      if (q < b_hi) sb[q - b_base] = __ldg(&br[q]);
+    }
+    return true;
+  };
+  long long tile = (long long)blockIdx.x * kTwWarps + wib;
+  int pa0, pb0, pal0, pbl0, pa1, pb1, pal1, pbl1;
+  load_ptrs(tile, pa0, pb0, pal0, pbl0);
+  load_ptrs(tile + nW, pa1, pb1, pal1, pbl1);
+  bool fit0 = tile < n_tiles ? issue(0, pa0, pb0, pal0, pbl0) : false;
+  unsigned phases = 0;  // bit s = the parity stage s's mbarrier completes next
+  for (int k = 0; tile < n_tiles; tile += nW, k++) {
+    const int stage = k & 1;
+    int pan, pbn, paln, pbln;
+    load_ptrs(tile + 2 * nW, pan, pbn, paln, pbln);
+    const bool fit1 = tile + nW < n_tiles ? issue(stage ^ 1, pa1, pb1, pal1, pbl1) : false;
+    const int a_base = __shfl_sync(0xffffffffu, pa0, 0) & ~3, b_base = __shfl_sync(0xffffffffu, pb0, 0) & ~3;
+    // this lane's pair
+    const int a0 = __shfl_sync(0xffffffffu, pa0, lc);
+    const int b0 = __shfl_sync(0xffffffffu, pb0, lc);
+    int a1 = __shfl_sync(0xffffffffu, pa0, (lc + 1) & 31);
+    int b1 = __shfl_sync(0xffffffffu, pb0, (lc + 1) & 31);
+    if (WC == 32 && lc == 31) {
+      a1 = pal0;
+      b1 = pbl0;
+    }
+    const int la = a1 - a0, lb = b1 - b0;
+    if (fit0) {
+      __syncwarp();  // the plain-loaded tail entries
+      mbar_wait(&S.bar[wib][stage], (phases >> stage) & 1u);
+      phases ^= 1u << stage;
+      const int* sa = S.buf[wib][stage][0];
+      const int* sb = S.buf[wib][stage][1];
+      const bool is_long = la > 0 && lb > 0 && la + lb > G * kTwLongPerLane;
+      if (la > 0 && lb > 0 && !is_long) {
+        const bool a_long = la >= lb;
+        const int* L = a_long ? sa + (a0 - a_base) : sb + (b0 - b_base);
+        const int* Sh = a_long ? sb + (b0 - b_base) : sa + (a0 - a_base);
+        const int ll = a_long ? la : lb, sl = a_long ? lb : la;
+        const int i0 = G == 1 ? 0 : (ll * sub) >> LG;  // ll <= kTwCap: 32-bit products
+        const int ie = G == 1 ? ll : (ll * (sub + 1)) >> LG;
+        if (i0 < ie) {
+          int l = L[i0];
+          const int j0 = (G == 1 || sub == 0) ? 0 : tt_lower_bound(Sh, sl, l);
+          if (j0 < sl) {
+            // two-pointer merge on shared-memory byte addresses; the inner loop runs
+            // to the next match or the end of either range with both cursors reloaded
+            // every step (a read one past a list's end stays inside the buffers)
+            const unsigned Lb = (unsigned)__cvta_generic_to_shared(L);
+            const unsigned Sb = (unsigned)__cvta_generic_to_shared(Sh);
+            unsigned pl = Lb + 4u * (unsigned)i0, ps = Sb + 4u * (unsigned)j0;
+            const unsigned ple = Lb + 4u * (unsigned)ie, pse = Sb + 4u * (unsigned)sl;
+            int s = tt_lds(ps);
+            int ln = tt_lds(pl + 4u), sn = tt_lds(ps + 4u);  // up to two entries past a list's end: inside the slack
+            for (;;) {
+              while (pl < ple && ps < pse && l != s) tt_step(pl, ps, l, s, ln, sn);
+              if (pl >= ple || ps >= pse) break;
+              const int i = (int)((pl - Lb) >> 2), j = (int)((ps - Sb) >> 2);
+              dd_add_match(acc, av, bv, a_long ? a0 + i : a0 + j, a_long ? b0 + j : b0 + i);
+              pl += 4u;
+              ps += 4u;
+              l = ln;
+              s = sn;
+              ln = tt_lds(pl + 4u);
+              sn = tt_lds(ps + 4u);
+            }
+          }
+        }
+      }
+      // pairs far above the mean length, in column order, by the whole warp
+      unsigned m = __ballot_sync(0xffffffffu, is_long && sub == 0);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const int xa0 = __shfl_sync(0xffffffffu, a0, src), xa1 = __shfl_sync(0xffffffffu, a1, src);
+        const int xb0 = __shfl_sync(0xffffffffu, b0, src), xb1 = __shfl_sync(0xffffffffu, b1, src);
+        tw_search_pair<false>(acc, lane, sa + (xa0 - a_base), sb + (xb0 - b_base), xa0, xa1, xb0, xb1, av, bv);
+      }
+    } else {
+      // runs beyond the buffers: pair by pair in global memory
+      for (int c = 0; c < WC; c++) {
+        const int src = c << LG;
+        const int xa0 = __shfl_sync(0xffffffffu, a0, src), xa1 = __shfl_sync(0xffffffffu, a1, src);
+        const int xb0 = __shfl_sync(0xffffffffu, b0, src), xb1 = __shfl_sync(0xffffffffu, b1, src);
+        tw_search_pair<true>(acc, lane, ar + xa0, br + xb0, xa0, xa1, xb0, xb1, av, bv);
+      }
+    }
+    __syncwarp();  // the stage's buffers are free for the copies of tile k + 2
+    pa0 = pa1, pb0 = pb1, pal0 = pal1, pbl0 = pbl1;
+    pa1 = pan, pb1 = pbn, pal1 = paln, pbl1 = pbln;
+    fit0 = fit1;
+  }
+  // deterministic block reduction, last block folds the partials
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc = dd_merge(acc, dd_shfl_xor(acc, o));
+  if (lane == 0) S.s_warp[wib] = acc;
+  __syncthreads();
+  if (wib == 0) {
+    DD v = lane < kTwWarps ? S.s_warp[lane] : DD{0.0, 0.0};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = dd_merge(v, dd_shfl_xor(v, o));
+    if (lane == 0) {
+      partials[blockIdx.x] = v;
+      __threadfence();
+      const unsigned prev = atomicAdd(done, 1u);
+      S.s_last = (prev == gridDim.x - 1);
+    }
+  }
+  __syncthreads();
+  if (S.s_last && wib == 0) {
+    __threadfence();
+    DD v{0.0, 0.0};
+    for (long long b = lane; b < gridDim.x; b += 32) {
+      DD p{__ldcg(&partials[b].s), __ldcg(&partials[b].e)};
+      v = dd_merge(v, p);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = dd_merge(v, dd_shfl_xor(v, o));
+    if (lane == 0) {
+      const double hi2 = __dadd_rn(v.s, v.e);
+      const double lo2 = __dsub_rn(v.e, __dsub_rn(hi2, v.s));
+      out[0] = hi2;
+      out[1] = lo2;
+    }
+  }
+}
+
+template <int LG>
+static int trace_tile_grid() {
+  static std::atomic<int> grid[kMaxDevices];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return -1;
+  if (grid[dev] == 0) {
+    int per_sm = 0, sms = 0;
+    if (cudaFuncSetAttribute(trace_warp_tile_kernel<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(TwSmem)) != cudaSuccess)
+      return -1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_warp_tile_kernel<LG>, kTwThreads, sizeof(TwSmem));
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid[dev] = std::max(1, per_sm * sms);
+  }
+  return grid[dev];
+}
+
+int g_trace_engine = 0;  // as_set_trace_engine: 0 automatic (tile kernel), 1 warp-per-column kernel
+
 static int trace_grid() {
   static std::atomic<int> grid[kMaxDevices];
   int dev = 0;
@@ -280,13 +591,57 @@ int as_trace_atb_f64(int64_t n_rows, int64_t n_cols, const int32_t* a_col_ptr, c
   cudaStream_t st = S(stream);
   AS_REQUIRE(n_cols >= 0 && n_rows >= 0, AS_ERR_SHAPE, "negative dimension");
   AS_REQUIRE(ws_bytes >= as_trace_workspace_bytes(n_cols, nnz_a, nnz_b), AS_ERR_ARG, "workspace too small");
-  const long long blocks = std::min(trace_grid(), 148 * 32);
   unsigned* done = (unsigned*)ws;
   DD* partials = (DD*)((char*)ws + 256);
   AS_CUDA_TRY(cudaMemsetAsync(done, 0, sizeof(unsigned), st));
+  // the warp-tile kernel's bulk copies need 16-byte aligned row arrays
+  const bool aligned = (((uintptr_t)a_row_idx | (uintptr_t)b_row_idx) & 15u) == 0;
+  const double mean = n_cols > 0 ? (double)(nnz_a + nnz_b) / (2.0 * (double)n_cols) : 0.0;
+  if (g_trace_engine == 0 && aligned && n_cols > 0 && mean <= (double)kTwMaxMean && nnz_a < INT_MAX &&
+      nnz_b < INT_MAX) {
+    // lanes per column pair: <= kTwPerLane entries of each list per lane at the mean column length
+    int lg = 0;
+    while (lg < 5 && (double)(kTwPerLane << lg) < mean) lg++;
+    int grid = -1;
+#define AS_TT_LAUNCH(LG)                                                                                          \
+  case LG:                                                                                                        \
+    grid = trace_tile_grid<LG>();                                                                                 \
+    if (grid > 0) {                                                                                               \
+      const long long tiles = (n_cols + (32 >> LG) - 1) / (32 >> LG);                                             \
+      const unsigned blocks =                                                                                     \
+          (unsigned)std::min<long long>(std::min(grid, 148 * 32), (tiles + kTwWarps - 1) / kTwWarps);             \
+      trace_warp_tile_kernel<LG><<<blocks, kTwThreads, sizeof(TwSmem), st>>>(                                     \
+          n_cols, a_col_ptr, a_row_idx, a_vals, b_col_ptr, b_row_idx, b_vals, (int)nnz_a, (int)nnz_b, partials,   \
+          done, out);                                                                                             \
+    }                                                                                                             \
+    break;
+    switch (lg) {
+      AS_TT_LAUNCH(0)
+      AS_TT_LAUNCH(1)
+      AS_TT_LAUNCH(2)
+      AS_TT_LAUNCH(3)
+      AS_TT_LAUNCH(4)
+      AS_TT_LAUNCH(5)
+    }
+#undef AS_TT_LAUNCH
+    if (grid > 0) {
+      AS_LAUNCH_CHECK();
+      return AS_OK;
+    }
+  }
+  const long long blocks = std::min(trace_grid(), 148 * 32);
   trace_partial_kernel<<<(unsigned)blocks, kTrThreads, 0, st>>>(n_cols, a_col_ptr, a_row_idx, a_vals, b_col_ptr,
                                                                 b_row_idx, b_vals, partials, done, out);
   AS_LAUNCH_CHECK();
+  return AS_OK;
+}
+
+int as_set_trace_engine(int engine) {
+  if (engine < 0 || engine > 1) {
+    as::set_error("trace engine must be 0 or 1, got %d", engine);
+    return AS_ERR_ARG;
+  }
+  as::g_trace_engine = engine;
   return AS_OK;
 }
 

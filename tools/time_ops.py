@@ -21,6 +21,9 @@ def main():
     def T(a, dt):
         return torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
 
+    if os.environ.get("AS_TRACE_ENGINE"):
+        from paper_1805_03380_b200 import _lib
+        _lib.check(_lib.lib().as_set_trace_engine(int(os.environ["AS_TRACE_ENGINE"])))
     for op in ops:
         if op in ("add", "spgemm", "trace"):
             n, _, A, B = synth.cfg4_trace_pair() if op == "trace" else synth.cfg5_pair()
