@@ -280,6 +280,10 @@ trace_partial_kernel(long long n_cols, const int* __restrict__ ap, const int* __
 #define AS_TW_CAP 576
 #define AS_TW_PER_LANE 13  // a warp tile holds <= 32 x 13 = 416 entries of each list at the mean: 72 % of a buffer
 #endif
+#ifndef AS_TW_ILP2
+#define AS_TW_ILP2 0  // measured on cfg 4: 51 us with two chains per lane vs 43 us with one (more instructions, more searches)
+#endif
+constexpr bool kTwIlp2 = AS_TW_ILP2 != 0;  // two interleaved chains per lane
 constexpr int kTwWarps = AS_TW_WARPS;  // warps per CTA
 constexpr int kTwThreads = kTwWarps * 32;
 constexpr int kTwCap = AS_TW_CAP;      // entries per list buffer of a warp
@@ -324,6 +328,47 @@ AS_DEVICE_INLINE void tt_step(unsigned& pl, unsigned& ps, int& l, int& s, int& l
       " @q1 add.u32 %0, %0, 4;\n @q2 add.u32 %1, %1, 4;\n"
       " @q1 ld.shared.b32 %4, [%0+4];\n @q2 ld.shared.b32 %5, [%1+4];\n}"
       : "+r"(pl), "+r"(ps), "+r"(l), "+r"(s), "+r"(ln), "+r"(sn));
+}
+
+// the same step under an activity flag (two chains interleaved in one loop:
+// a finished chain stands still)
+AS_DEVICE_INLINE void tt_step_if(unsigned& pl, unsigned& ps, int& l, int& s, int& ln, int& sn, int act) {
+  asm volatile(
+      "{\n .reg .pred q0, q1, q2;\n setp.ne.s32 q0, %6, 0;\n"
+      " setp.lt.and.s32 q1, %2, %3, q0;\n setp.lt.and.s32 q2, %3, %2, q0;\n"
+      " @q1 mov.b32 %2, %4;\n @q2 mov.b32 %3, %5;\n"
+      " @q1 add.u32 %0, %0, 4;\n @q2 add.u32 %1, %1, 4;\n"
+      " @q1 ld.shared.b32 %4, [%0+4];\n @q2 ld.shared.b32 %5, [%1+4];\n}"
+      : "+r"(pl), "+r"(ps), "+r"(l), "+r"(s), "+r"(ln), "+r"(sn)
+      : "r"(act));
+}
+
+struct TtChain {  // one lane's merge of a segment of the longer list against the shorter one
+  unsigned pl, ps, ple, pse;
+  int l, s, ln, sn;
+};
+
+// chain over segment `seg` of `nseg` of L (ll entries) against Sh (sl entries); inert when empty
+AS_DEVICE_INLINE void tt_chain_init(TtChain& c, const int* L, const int* Sh, unsigned Lb, unsigned Sb, int ll, int sl,
+                                    int seg, int lg_nseg) {
+  c.pl = c.ple = c.ps = c.pse = 0u;
+  c.l = c.ln = 0;
+  c.s = c.sn = 1;
+  const int i0 = (ll * seg) >> lg_nseg, ie = (ll * (seg + 1)) >> lg_nseg;
+  if (i0 < ie) {
+    const int l = L[i0];
+    const int j0 = seg == 0 ? 0 : tt_lower_bound(Sh, sl, l);
+    if (j0 < sl) {
+      c.pl = Lb + 4u * (unsigned)i0;
+      c.ple = Lb + 4u * (unsigned)ie;
+      c.ps = Sb + 4u * (unsigned)j0;
+      c.pse = Sb + 4u * (unsigned)sl;
+      c.l = l;
+      c.s = tt_lds(c.ps);
+      c.ln = tt_lds(c.pl + 4u);  // up to two entries past a list's end: inside the slack
+      c.sn = tt_lds(c.ps + 4u);
+    }
+  }
 }
 
 // every entry of the shorter list (a stride per lane) searched in the longer one
@@ -451,33 +496,45 @@ trace_warp_tile_kernel(long long n_cols, const int* __restrict__ ap, const int* 
         const int* L = a_long ? sa + (a0 - a_base) : sb + (b0 - b_base);
         const int* Sh = a_long ? sb + (b0 - b_base) : sa + (a0 - a_base);
         const int ll = a_long ? la : lb, sl = a_long ? lb : la;
-        const int i0 = G == 1 ? 0 : (ll * sub) >> LG;  // ll <= kTwCap: 32-bit products
-        const int ie = G == 1 ? ll : (ll * (sub + 1)) >> LG;
-        if (i0 < ie) {
-          int l = L[i0];
-          const int j0 = (G == 1 || sub == 0) ? 0 : tt_lower_bound(Sh, sl, l);
-          if (j0 < sl) {
-            // two-pointer merge on shared-memory byte addresses; the inner loop runs
-            // to the next match or the end of either range with both cursors reloaded
-            // every step (a read one past a list's end stays inside the buffers)
-            const unsigned Lb = (unsigned)__cvta_generic_to_shared(L);
-            const unsigned Sb = (unsigned)__cvta_generic_to_shared(Sh);
-            unsigned pl = Lb + 4u * (unsigned)i0, ps = Sb + 4u * (unsigned)j0;
-            const unsigned ple = Lb + 4u * (unsigned)ie, pse = Sb + 4u * (unsigned)sl;
-            int s = tt_lds(ps);
-            int ln = tt_lds(pl + 4u), sn = tt_lds(ps + 4u);  // up to two entries past a list's end: inside the slack
-            for (;;) {
-              while (pl < ple && ps < pse && l != s) tt_step(pl, ps, l, s, ln, sn);
-              if (pl >= ple || ps >= pse) break;
-              const int i = (int)((pl - Lb) >> 2), j = (int)((ps - Sb) >> 2);
-              dd_add_match(acc, av, bv, a_long ? a0 + i : a0 + j, a_long ? b0 + j : b0 + i);
-              pl += 4u;
-              ps += 4u;
-              l = ln;
-              s = sn;
-              ln = tt_lds(pl + 4u);
-              sn = tt_lds(ps + 4u);
+        const unsigned Lb = (unsigned)__cvta_generic_to_shared(L);
+        const unsigned Sb = (unsigned)__cvta_generic_to_shared(Sh);
+        auto match = [&](TtChain& c) {
+          const int i = (int)((c.pl - Lb) >> 2), j = (int)((c.ps - Sb) >> 2);
+          dd_add_match(acc, av, bv, a_long ? a0 + i : a0 + j, a_long ? b0 + j : b0 + i);
+          c.pl += 4u;
+          c.ps += 4u;
+          c.l = c.ln;
+          c.s = c.sn;
+          c.ln = tt_lds(c.pl + 4u);
+          c.sn = tt_lds(c.ps + 4u);
+        };
+        if (kTwIlp2 && LG >= 1) {
+          // two chains per lane (2G segments per pair), interleaved in one loop: twice the
+          // independent compare -> move chains per warp for the same shared memory
+          TtChain c1, c2;
+          tt_chain_init(c1, L, Sh, Lb, Sb, ll, sl, 2 * sub, LG + 1);
+          tt_chain_init(c2, L, Sh, Lb, Sb, ll, sl, 2 * sub + 1, LG + 1);
+          for (;;) {
+            const bool act1 = c1.pl < c1.ple && c1.ps < c1.pse, act2 = c2.pl < c2.ple && c2.ps < c2.pse;
+            if (!(act1 || act2)) break;
+            const bool m1 = act1 && c1.l == c1.s, m2 = act2 && c2.l == c2.s;
+            if (m1 || m2) {
+              if (m1) match(c1);
+              if (m2) match(c2);
+              continue;
             }
+            tt_step_if(c1.pl, c1.ps, c1.l, c1.s, c1.ln, c1.sn, act1);
+            tt_step_if(c2.pl, c2.ps, c2.l, c2.s, c2.ln, c2.sn, act2);
+          }
+        } else {
+          // two-pointer merge on shared-memory byte addresses; the inner loop runs to the
+          // next match or the end of either range
+          TtChain c;
+          tt_chain_init(c, L, Sh, Lb, Sb, ll, sl, sub, LG);
+          for (;;) {
+            while (c.pl < c.ple && c.ps < c.pse && c.l != c.s) tt_step(c.pl, c.ps, c.l, c.s, c.ln, c.sn);
+            if (c.pl >= c.ple || c.ps >= c.pse) break;
+            match(c);
           }
         }
       }
