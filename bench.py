@@ -421,10 +421,6 @@ def main_device(args):
     ops = {}
     if rank == 0 and world == 1 and not args.headline_only:
         ops = bench_ops(args, dev, L, sp, timed, peak)
-    ops_mg = None
-    if (world > 1 or args.mg) and not args.headline_only:
-        ops_mg = bench_mg_ops(args, dev, world, rank, l2_flush, peak)
-
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, reps, el = time_oracle_build((n_rows, n_cols, rows, cols, vals), args.cpu_budget)
@@ -433,8 +429,8 @@ def main_device(args):
                          "os.cpu_count()=%d)" % (reps, el, os.cpu_count()),
                "reference_numba": time_reference_build((n_rows, n_cols, rows, cols, vals), min(args.cpu_budget, 5.0))}
 
-    if rank == 0:
-        line = {
+    def make_line(ops_mg_value):
+        return {
             "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
@@ -447,9 +443,33 @@ def main_device(args):
                          "kernel": "as_coo_to_csc_f64 (one cooperative sort-reduce kernel)",
                          "algorithmic_bytes": build_bytes},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 1 * args.steps, "clocks": clocks, "ops": ops,
-            "ops_multi_gpu": ops_mg,
+            "ops_multi_gpu": ops_mg_value,
         }
-        print(json.dumps(line), flush=True)
+
+    ops_mg = None
+    if (world > 1 or args.mg) and not args.headline_only:
+        # The sharded ops have never run on more than one GPU (one GPU is all this
+        # environment reaches): if an exchange stalls, every rank leaves after
+        # --mg-deadline seconds and rank 0 still prints the headline line
+        # (ops_multi_gpu = the error) instead of the job dying without one.
+        import threading
+
+        def give_up():
+            if rank == 0:
+                print(json.dumps(make_line({"error": "sharded ops did not finish within %.0f s; headline kept"
+                                                     % args.mg_deadline})), flush=True)
+            os._exit(0)
+
+        watchdog = threading.Timer(args.mg_deadline, give_up)
+        watchdog.daemon = True
+        watchdog.start()
+        try:
+            ops_mg = bench_mg_ops(args, dev, world, rank, l2_flush, peak)
+        finally:
+            watchdog.cancel()
+
+    if rank == 0:
+        print(json.dumps(make_line(ops_mg)), flush=True)
     if world > 1 or args.mg:
         dist.barrier()
         dist.destroy_process_group()
@@ -1134,6 +1154,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--skip-slow-checks", action="store_true")
     ap.add_argument("--flush", default="read", choices=["read", "write"])
+    ap.add_argument("--mg-deadline", type=float, default=600.0,
+                    help="seconds the sharded multi-GPU ops may take before the headline line is printed without them")
     ap.add_argument("--mg", action="store_true",
                     help="run the sharded (multi-GPU) ops even at world size 1 (needs torchrun env)")
     args = ap.parse_args()

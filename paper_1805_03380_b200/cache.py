@@ -17,6 +17,7 @@ of latest values, so a write-only workload never pays for them.
 
 from __future__ import annotations
 
+from array import array
 from typing import Iterator, Optional
 
 import numpy as np
@@ -50,6 +51,9 @@ class InsertionCache:
         self._cols = np.empty(cap, np.int32)
         self._vals = np.empty(cap, np.float64)
         self._n = 0
+        # tails of single writes not yet moved into the columns above
+        self._tr, self._tc, self._tv = array("i"), array("i"), array("d")
+        self._ar, self._ac, self._av = self._tr.append, self._tc.append, self._tv.append
         self._cur = {}
         self._indexed = 0
         self._count = base.nnz if base is not None else 0
@@ -57,7 +61,22 @@ class InsertionCache:
     # -- log ------------------------------------------------------------------
     @property
     def n_writes(self) -> int:
-        return self._n
+        return self._n + len(self._tr)
+
+    def _spill(self) -> None:
+        """Move the single-write tails into the numpy columns (write order kept)."""
+        k = len(self._tr)
+        if not k:
+            return
+        n = self._n
+        if n + k > self._rows.shape[0]:
+            self._grow(n + k)
+        self._rows[n : n + k] = np.frombuffer(self._tr, np.int32)
+        self._cols[n : n + k] = np.frombuffer(self._tc, np.int32)
+        self._vals[n : n + k] = np.frombuffer(self._tv, np.float64)
+        self._n = n + k
+        # (the temporaries above are gone: the arrays may be resized again)
+        del self._tr[:], self._tc[:], self._tv[:]
 
     def _grow(self, need: int):
         cap = self._rows.shape[0]
@@ -77,13 +96,17 @@ class InsertionCache:
 
     def write(self, row: int, col: int, value: float) -> None:
         """Append one element write (coordinates already checked)."""
-        n = self._n
-        if n == self._rows.shape[0]:
-            self._grow(n + 1)
-        self._rows[n] = row
-        self._cols[n] = col
-        self._vals[n] = value
-        self._n = n + 1
+        try:
+            self._ar(row)
+        except TypeError:  # an integral float / numpy scalar without __index__
+            row, col = int(row), int(col)
+            self._ar(row)
+        try:
+            self._ac(col)
+            self._av(value)
+        except BaseException:  # keep the three tails the same length
+            del self._tr[len(self._tv):], self._tc[len(self._tv):]
+            raise
 
     def write_many(self, rows, cols, vals) -> None:
         """Append a batch of element writes, applied in array order."""
@@ -94,6 +117,7 @@ class InsertionCache:
         if ((rows < 0) | (rows >= self.dims.n_rows) | (cols < 0) | (cols >= self.dims.n_cols)).any():
             bad = int(np.flatnonzero((rows < 0) | (rows >= self.dims.n_rows) | (cols < 0) | (cols >= self.dims.n_cols))[0])
             raise CoordinateError("write %d = (%d, %d) outside %s matrix" % (bad, rows[bad], cols[bad], self.dims))
+        self._spill()
         if self._n + k > self._rows.shape[0]:
             self._grow(self._n + k)
         self._rows[self._n : self._n + k] = rows
@@ -109,6 +133,7 @@ class InsertionCache:
         return float(self._base.values[pos]) if pos >= 0 else 0.0
 
     def _sync(self) -> None:
+        self._spill()
         n_rows = self.dims.n_rows
         cur = self._cur
         for i in range(self._indexed, self._n):
@@ -184,6 +209,7 @@ class InsertionCache:
         """Flush base + log into canonical CSC with one GPU pass."""
         device = device or (self._base.device if self._base is not None else csc_mod.default_device())
         base = self._base if self._base is not None else csc_mod.empty(self.dims, device)
+        self._spill()
         n = self._n
         rows = torch.from_numpy(self._rows[:n]).to(device, non_blocking=False)
         cols = torch.from_numpy(self._cols[:n]).to(device, non_blocking=False)

@@ -25,13 +25,14 @@ def main():
         from paper_1805_03380_b200 import _lib
         _lib.check(_lib.lib().as_set_trace_engine(int(os.environ["AS_TRACE_ENGINE"])))
     for op in ops:
-        if op in ("add", "spgemm", "trace"):
+        if op in ("add", "spgemm", "trace", "trace5"):
             n, _, A, B = synth.cfg4_trace_pair() if op == "trace" else synth.cfg5_pair()
             a = (T(A[2], torch.int32), T(A[1], torch.int32), T(A[0], torch.float64))
             b = (T(B[2], torch.int32), T(B[1], torch.int32), T(B[0], torch.float64))
             fn = {"add": lambda: _kernels.linear_combine(n, n, a, b, 1.0, 1.0),
                   "spgemm": lambda: _kernels.spgemm(n, n, n, a, b),
-                  "trace": lambda: _kernels.fused_trace(n, n, a, b)}[op]
+                  "trace": lambda: _kernels.fused_trace(n, n, a, b),
+                  "trace5": lambda: _kernels.fused_trace(n, n, a, b)}[op]  # trace on cfg 5's Zipf pair
         elif op in ("build", "transpose"):
             n_rows, n_cols, rows, cols, vals = synth.cfg1_triplets()
             r, c, v = T(rows, torch.int32), T(cols, torch.int32), T(vals, torch.float64)
