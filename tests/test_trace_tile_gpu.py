@@ -81,7 +81,9 @@ def test_long_and_oversized_columns(K, engine):
     n_rows = 40_000
     g = np.random.default_rng(7)
     lens = g.poisson(8, 4000)
-    lens[100:140] = 700            # tiles far beyond the buffers
+    lens[100:140] = 700            # tiles far beyond the buffers: every pair alone exceeds them
+    lens[300:340] = 100            # tiles beyond the buffers made of pairs that would fit alone
+    lens[400:420:3] = 400
     lens[900] = 3000
     lens[901] = 0
     lens[1500] = 12_000
