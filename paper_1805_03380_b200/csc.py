@@ -11,6 +11,7 @@ mirror, bulk work runs on the device.
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass
 from typing import Iterator, NamedTuple, Sequence
 
@@ -67,6 +68,22 @@ def _to_dev(a, dtype, device):
     if isinstance(a, torch.Tensor):
         return a.to(device=device, dtype=dtype, non_blocking=True).contiguous()
     return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(device, non_blocking=True)
+
+
+_STAGING_LOCK = threading.Lock()
+_STAGING = {}
+
+
+def _staging(n_ptr: int, cap: int, val_dtype):
+    """Process-wide pinned read-back buffers (grow-only) for the host mirror."""
+    def grown(key, n, dtype):
+        t = _STAGING.get(key)
+        if t is None or t.shape[0] < n:
+            t = _STAGING[key] = torch.empty(max(n, 1) + max(n, 1) // 4, dtype=dtype, pin_memory=True)
+        return t
+
+    return (grown("ptr", n_ptr, torch.int32)[:n_ptr], grown("rows", cap, torch.int32),
+            grown(("vals", val_dtype), cap, val_dtype))
 
 
 class CscData:
@@ -139,9 +156,9 @@ class CscData:
         pend = self._pend is not None
         ri, vv = self._row_idx, self._vals  # full capacity while pending
         if out is None:
-            out = (torch.empty(self.col_ptr.shape[0], dtype=torch.int32).pin_memory(),
-                   torch.empty(ri.shape[0], dtype=torch.int32).pin_memory(),
-                   torch.empty(vv.shape[0], dtype=vv.dtype).pin_memory())
+            out = (torch.empty(self.col_ptr.shape[0], dtype=torch.int32, pin_memory=True),
+                   torch.empty(ri.shape[0], dtype=torch.int32, pin_memory=True),
+                   torch.empty(vv.shape[0], dtype=vv.dtype, pin_memory=True))
         o_ptr, o_rows, o_vals = out
         stream = torch.cuda.current_stream(self.col_ptr.device)
         o_ptr.copy_(self.col_ptr, non_blocking=True)
@@ -203,8 +220,18 @@ class CscData:
     # -- reference-typed host mirror (csc.py:54-67) -----------------------------
     def _mirror(self):
         if self._host is None:
-            p, r, v = self.to_host()
-            self._host = (v.numpy().astype(np.float64), r.numpy().astype(np.int64), p.numpy().astype(np.int64))
+            if self.col_ptr.device.type == "cpu":
+                p, r, v = self.to_host()
+                self._host = (v.numpy().astype(np.float64), r.numpy().astype(np.int64), p.numpy().astype(np.int64))
+            else:
+                # the copies land in pinned staging buffers kept for the process (a fresh
+                # pinned allocation per read-back cost 3-4 ms at cfg 2's size); the
+                # reference-typed arrays below are copies, so the buffers are free again
+                with _STAGING_LOCK:
+                    p, r, v = self.to_host(out=_staging(self.col_ptr.shape[0], self._row_idx.shape[0],
+                                                        self._vals.dtype))
+                    self._host = (v.numpy().astype(np.float64), r.numpy().astype(np.int64),
+                                  p.numpy().astype(np.int64))
         return self._host
 
     @property
