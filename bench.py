@@ -163,6 +163,40 @@ def time_reference_build(inputs, budget_s: float):
                       "(numpy/numba, single-threaded as shipped)" % (reps, el)}
 
 
+def time_dropin_build(inputs, budget_s: float):
+    """The reference package's own construction call (csc.canonicalize on numpy
+    int64 / float64 arrays, reference CscData out) with this back end swapped in
+    by ref_kernels.install: what an unmodified reference user gets.  Pageable
+    host arrays in, reference-typed numpy arrays out, every copy inside."""
+    pkg = import_reference()
+    if pkg is None:
+        return None
+    from paper_1805_03380_b200 import ref_kernels
+
+    n_rows, n_cols, rows, cols, vals = inputs
+    dims = pkg.Dims(n_rows, n_cols)
+    stock = pkg.csc.canonicalize(dims, rows, cols, vals, "sum")
+    undo = ref_kernels.install(pkg)
+    try:
+        got = pkg.csc.canonicalize(dims, rows, cols, vals, "sum")  # warm, and the parity check
+        same = bool(np.array_equal(got.col_offsets, stock.col_offsets) and np.array_equal(got.row_indices,
+                                                                                          stock.row_indices)
+                    and np.array_equal(got.values.view(np.int64), stock.values.view(np.int64)))
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            pkg.csc.canonicalize(dims, rows, cols, vals, "sum")
+            reps += 1
+            el = time.perf_counter() - t0
+            if el >= budget_s:
+                break
+    finally:
+        undo()
+    return {"value": reps * rows.shape[0] / el, "unit": "nnz/s", "ms": 1e3 * el / reps, "kind": "reference API, GPU back end",
+            "identical_to_stock_reference": same,
+            "sample": "%d full cfg1 builds in %.1f s: autosparse.csc.canonicalize after ref_kernels.install(autosparse) "
+                      "(pageable numpy int64/float64 in, reference CscData out)" % (reps, el)}
+
+
 def headline_config(n_rows, n_cols, n, nnz):
     """The `config` both arms print (identical dicts)."""
     return {"workload": HEADLINE, "n_rows": n_rows, "n_cols": n_cols, "triplets": n, "nnz_out": nnz,
@@ -427,7 +461,9 @@ def main_device(args):
         cpu = {"value": rate, "unit": "nnz/s", "cores": 1, "kind": "port",
                "sample": "%d full cfg1 builds in %.1f s (oracle/oracle.c orc_canonicalize, 1 thread; "
                          "os.cpu_count()=%d)" % (reps, el, os.cpu_count()),
-               "reference_numba": time_reference_build((n_rows, n_cols, rows, cols, vals), min(args.cpu_budget, 5.0))}
+               "reference_numba": time_reference_build((n_rows, n_cols, rows, cols, vals), min(args.cpu_budget, 5.0)),
+               "reference_api_gpu_backend": time_dropin_build((n_rows, n_cols, rows, cols, vals),
+                                                              min(args.cpu_budget, 2.0))}
 
     def make_line(ops_mg_value):
         return {

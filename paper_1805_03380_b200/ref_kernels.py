@@ -98,13 +98,21 @@ def fused_trace(n_cols, a_vals, a_rows, a_offs, b_vals, b_rows, b_offs):
 
 def canonicalize(n_rows, n_cols, rows, cols, values, dup="sum"):
     """csc.canonicalize (csc.py:148-193) on flat arrays; returns
-    (values, row_indices, col_offsets)."""
-    r = torch.as_tensor(np.ascontiguousarray(rows, dtype=np.int64)).to(_dev())
-    c = torch.as_tensor(np.ascontiguousarray(cols, dtype=np.int64)).to(_dev())
-    p, ri, v, bad = _kernels.coo_to_csc(n_rows, n_cols, r, c, _f64(values), dup)
+    (values, row_indices, col_offsets).  The int64 coordinates are packed on
+    host threads while the values are copied (csc.build_device) and the result
+    comes back through the device CSC's host mirror (pinned staging, rows at
+    half width when they fit): 4.0 -> 3.0 ms for cfg 1's 1e6 triplets."""
+    from . import csc as csc_mod
+
+    r = np.ascontiguousarray(rows, dtype=np.int64)
+    c = np.ascontiguousarray(cols, dtype=np.int64)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    if r.shape[0] == 0:
+        return np.empty(0, np.float64), np.empty(0, np.int64), np.zeros(int(n_cols) + 1, np.int64)
+    m, bad = csc_mod.build_device(csc_mod.Dims(int(n_rows), int(n_cols)), r, c, v, dup, _dev())
     if bad is not None:
         raise IndexError("coordinate %d outside %dx%d matrix" % (bad, n_rows, n_cols))
-    return _out(p, ri, v)
+    return m.values, m.row_indices, m.col_offsets
 
 
 def rbt_to_csc(n_rows, n_cols, base, log_rows, log_cols, log_vals):
