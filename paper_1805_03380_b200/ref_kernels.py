@@ -47,10 +47,14 @@ def _csc(vals, rows, offs):
     return _i32(offs), _i32(rows), _f64(vals)
 
 
-def _out(p, r, v):
+def _out(p, r, v, n_rows=None):
     """(values f64, row_indices i64, col_offsets i64) numpy, the reference's
-    return order."""
-    return v.cpu().numpy().astype(np.float64), r.cpu().numpy().astype(np.int64), p.cpu().numpy().astype(np.int64)
+    return order, read back through the device CSC's host mirror (pinned
+    staging kept for the process; rows at half width when n_rows <= 65536)."""
+    from .csc import DEVICE_INDEX_MAX, CscData, Dims
+
+    d = CscData(Dims(int(n_rows) if n_rows is not None else DEVICE_INDEX_MAX, int(p.shape[0]) - 1), p, r, v)
+    return d.values, d.row_indices, d.col_offsets
 
 
 def linear_combine(n_cols, a_vals, a_rows, a_offs, b_vals, b_rows, b_offs, alpha, beta):
@@ -58,7 +62,7 @@ def linear_combine(n_cols, a_vals, a_rows, a_offs, b_vals, b_rows, b_offs, alpha
     n_rows = int(max(np.max(a_rows, initial=-1), np.max(b_rows, initial=-1)) + 1)
     p, r, v = _kernels.linear_combine(n_rows, n_cols, _csc(a_vals, a_rows, a_offs), _csc(b_vals, b_rows, b_offs),
                                       alpha, beta)
-    return _out(p, r, v)
+    return _out(p, r, v, n_rows)
 
 
 def spgemm(n_rows_a, a_vals, a_rows, a_offs, b_vals, b_rows, b_offs, n_cols_b):
@@ -66,7 +70,7 @@ def spgemm(n_rows_a, a_vals, a_rows, a_offs, b_vals, b_rows, b_offs, n_cols_b):
     n_inner = int(np.asarray(a_offs).shape[0] - 1)
     p, r, v = _kernels.spgemm(n_rows_a, n_inner, n_cols_b, _csc(a_vals, a_rows, a_offs),
                               _csc(b_vals, b_rows, b_offs))
-    return _out(p, r, v)
+    return _out(p, r, v, n_rows_a)
 
 
 def vec_times_mat(v, vals, rows, offs, n_cols):
@@ -86,7 +90,7 @@ def mat_times_vec(vals, rows, offs, x, n_rows, n_cols):
 
 def transpose(n_rows, n_cols, vals, rows, offs):
     """_kernels.transpose (_kernels.py:130-150)."""
-    return _out(*_kernels.transpose(n_rows, n_cols, *_csc(vals, rows, offs)))
+    return _out(*_kernels.transpose(n_rows, n_cols, *_csc(vals, rows, offs)), n_cols)
 
 
 def fused_trace(n_cols, a_vals, a_rows, a_offs, b_vals, b_rows, b_offs):
@@ -101,7 +105,7 @@ def canonicalize(n_rows, n_cols, rows, cols, values, dup="sum"):
     (values, row_indices, col_offsets).  The int64 coordinates are packed on
     host threads while the values are copied (csc.build_device) and the result
     comes back through the device CSC's host mirror (pinned staging, rows at
-    half width when they fit): 4.0 -> 3.0 ms for cfg 1's 1e6 triplets."""
+    half width when they fit)."""
     from . import csc as csc_mod
 
     r = np.ascontiguousarray(rows, dtype=np.int64)
@@ -121,7 +125,7 @@ def rbt_to_csc(n_rows, n_cols, base, log_rows, log_cols, log_vals):
     p, r, v, bad = _kernels.flush_log(n_rows, n_cols, _csc(*base), _i32(log_rows), _i32(log_cols), _f64(log_vals))
     if bad is not None:
         raise IndexError("write %d outside %dx%d matrix" % (bad, n_rows, n_cols))
-    return _out(p, r, v)
+    return _out(p, r, v, n_rows)
 
 
 # ---------------------------------------------------------------------------
