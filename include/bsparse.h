@@ -219,6 +219,40 @@ int as_trace_atb_f64(int64_t n_rows, int64_t n_cols, const int32_t *a_col_ptr, c
 int as_set_trace_engine(int engine);
 
 /* ---------------------------------------------------------------------------
+ * Multi-GPU (no reference counterpart): one process per GPU.
+ * The caller creates the NCCL communicator (ncclCommInitRank, or the one its
+ * framework owns) and hands it over; NCCL's entry points are resolved at run
+ * time from the libnccl the process has loaded (`nccl_library`: a path to try
+ * first, or NULL for libnccl.so.2), so the library has no link-time
+ * dependency on NCCL.  Each as_mg_* op is the rank-local kernel followed by
+ * its collective on the caller's stream; paper_1805_03380_b200/dist.py is the
+ * torch.distributed twin (and does SpGEMM, whose variable-size exchange needs
+ * host-side sizing).
+ *
+ * as_mg_trace_atb_f64: trace(A^T B) over this rank's columns [c0, c1) (full
+ *   A and B on every rank; dist.trace_shard balances the ranges), then an
+ *   all-gather of the ranks' (sum, residual) pairs combined in rank order with
+ *   TwoSum carries: every rank gets the same out[0..1], independent of the
+ *   reduction tree.  ws: as_mg_trace_workspace_bytes.
+ * as_mg_spmm_csr_f32: C = A @ B with A's CSR replicated and the k dense
+ *   columns split evenly (k % world == 0, ldc == n_rows): rank r multiplies
+ *   columns [r k / world, (r + 1) k / world) and the blocks are all-gathered
+ *   in place into every rank's C.  ws: as_spmm_workspace_bytes.
+ */
+int as_mg_init(void *nccl_comm, int rank, int world, const char *nccl_library);
+int as_mg_shutdown(void);
+int as_mg_rank(void);
+int as_mg_world(void);
+size_t as_mg_trace_workspace_bytes(int64_t n_cols, int64_t nnz_a, int64_t nnz_b, int world);
+int as_mg_trace_atb_f64(int64_t n_rows, int64_t n_cols, const int32_t *a_col_ptr, const int32_t *a_row_idx,
+                        const double *a_vals, const int32_t *b_col_ptr, const int32_t *b_row_idx,
+                        const double *b_vals, int64_t nnz_a, int64_t nnz_b, int64_t c0, int64_t c1, double *out,
+                        void *ws, size_t ws_bytes, void *stream);
+int as_mg_spmm_csr_f32(int64_t n_rows, int64_t n_cols, int64_t k, const int32_t *row_ptr, const int32_t *col_idx,
+                       const float *vals, const float *B, int64_t ldb, float *C, int64_t ldc, void *ws,
+                       size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
  * construction-funnelled ops and segmented reductions of the
  * reference's ops module (csrc/funnel.cu).
  *

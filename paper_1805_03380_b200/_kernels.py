@@ -288,6 +288,54 @@ def spmm(n_rows, n_cols, csr, B, exact=None, out=None):
     return C
 
 
+# ---------------------------------------------------------------------------
+# Multi-GPU entry points of the C ABI (csrc/mg.cu): the rank-local kernel and
+# its NCCL collective in one call, on a communicator the caller owns.
+# (dist.py drives the same ops through torch.distributed.)
+
+def mg_init(nccl_comm: int, rank: int, world: int, nccl_library: str = None) -> None:
+    """Hand the process's ncclComm_t (an integer address) to the library."""
+    lib_path = nccl_library.encode() if nccl_library else None
+    check(_lib.lib().as_mg_init(nccl_comm, rank, world, lib_path))
+
+
+def mg_shutdown() -> None:
+    check(_lib.lib().as_mg_shutdown())
+
+
+def mg_fused_trace(n_rows, n_cols, a, b, c0, c1, out=None):
+    """trace(A^T B): this rank's columns [c0, c1), all-gathered and combined in
+    rank order; device tensor [sum, residual], identical on every rank."""
+    L = _lib.lib()
+    a_ptr, a_rows, a_vals = a
+    b_ptr, b_rows, b_vals = b
+    dev = a_ptr.device
+    na, nb = int(a_rows.shape[0]), int(b_rows.shape[0])
+    if out is None:
+        out = torch.empty(2, dtype=torch.float64, device=dev)
+    ws_bytes = L.as_mg_trace_workspace_bytes(n_cols, na, nb, L.as_mg_world())
+    ws = workspace(ws_bytes, dev)
+    check(L.as_mg_trace_atb_f64(n_rows, n_cols, ptr(a_ptr), ptr(a_rows), ptr(a_vals), ptr(b_ptr), ptr(b_rows),
+                                ptr(b_vals), na, nb, c0, c1, ptr(out), ptr(ws), ws_bytes, stream()))
+    return out
+
+
+def mg_spmm(n_rows, n_cols, csr, B, out=None):
+    """C = A @ B (float32): this rank's block of the dense columns, then an
+    in-place all-gather into every rank's packed column-major C."""
+    L = _lib.lib()
+    r_ptr, c_idx, vals = csr
+    dev = r_ptr.device
+    B, ldb = as_col_major(B)
+    k = int(B.shape[1])
+    C = torch.empty((k, n_rows), dtype=torch.float32, device=dev).t() if out is None else out
+    ws_bytes = L.as_spmm_workspace_bytes(n_cols, k, 4)
+    ws = workspace(ws_bytes, dev)
+    check(L.as_mg_spmm_csr_f32(n_rows, n_cols, k, ptr(r_ptr), ptr(c_idx), ptr(vals), ptr(B), ldb, ptr(C), n_rows,
+                               ptr(ws), ws_bytes, stream()))
+    return C
+
+
 def spmm_csc(n_rows, n_cols, csc, B, out=None):
     """C = A @ B straight over the CSC of A (column-merge, float32; no CSR
     needed): the reference's loop order (_kernels.mat_times_vec,

@@ -54,6 +54,13 @@ SIGNATURES = {
     "as_spmm_csc_f32": (INT, [I64, I64, I64, I64, P, P, P, P, I64, P, I64, P, SZ, P]),
     "as_vecmat_csc_f64": (INT, [I64, I64, P, P, P, P, P, P]),
     "as_set_trace_engine": (INT, [INT]),
+    "as_mg_init": (INT, [P, INT, INT, ctypes.c_char_p]),
+    "as_mg_shutdown": (INT, []),
+    "as_mg_rank": (INT, []),
+    "as_mg_world": (INT, []),
+    "as_mg_trace_workspace_bytes": (SZ, [I64, I64, I64, INT]),
+    "as_mg_trace_atb_f64": (INT, [I64, I64, P, P, P, P, P, P, I64, I64, I64, I64, P, P, SZ, P]),
+    "as_mg_spmm_csr_f32": (INT, [I64, I64, I64, P, P, P, P, I64, P, I64, P, SZ, P]),
     "as_trace_workspace_bytes": (SZ, [I64, I64, I64]),
     "as_trace_atb_f64": (INT, [I64, I64, P, P, P, P, P, P, I64, I64, P, P, SZ, P]),
     "as_expand_cols": (INT, [I64, P, P, P]),
