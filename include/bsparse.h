@@ -226,8 +226,8 @@ int as_set_trace_engine(int engine);
  * first, or NULL for libnccl.so.2), so the library has no link-time
  * dependency on NCCL.  Each as_mg_* op is the rank-local kernel followed by
  * its collective on the caller's stream; paper_1805_03380_b200/dist.py is the
- * torch.distributed twin (and does SpGEMM, whose variable-size exchange needs
- * host-side sizing).
+ * torch.distributed twin (it also gathers SpGEMM slices onto one rank, whose
+ * variable-size exchange needs host-side sizing).
  *
  * as_mg_trace_atb_f64: trace(A^T B) over this rank's columns [c0, c1) (full
  *   A and B on every rank; dist.trace_shard balances the ranges), then an
@@ -238,6 +238,11 @@ int as_set_trace_engine(int engine);
  *   columns split evenly (k % world == 0, ldc == n_rows): rank r multiplies
  *   columns [r k / world, (r + 1) k / world) and the blocks are all-gathered
  *   in place into every rank's C.  ws: as_spmm_workspace_bytes.
+ * as_mg_spgemm_f64: as_spgemm_f64 on this rank's standalone column slice of B
+ *   (dist.spgemm_shard: ranges of equal Gustavson products; A replicated),
+ *   then one all-gather of the slices' nnz: slice_nnz[world] (device) and
+ *   slice_offset[0] = this slice's first element in the concatenation of all
+ *   slices.  C stays distributed (dist.DistCsc); nothing is read on the host.
  */
 int as_mg_init(void *nccl_comm, int rank, int world, const char *nccl_library);
 int as_mg_shutdown(void);
@@ -251,6 +256,12 @@ int as_mg_trace_atb_f64(int64_t n_rows, int64_t n_cols, const int32_t *a_col_ptr
 int as_mg_spmm_csr_f32(int64_t n_rows, int64_t n_cols, int64_t k, const int32_t *row_ptr, const int32_t *col_idx,
                        const float *vals, const float *B, int64_t ldb, float *C, int64_t ldc, void *ws,
                        size_t ws_bytes, void *stream);
+int as_mg_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int32_t *a_col_ptr,
+                     const int32_t *a_row_idx, const double *a_vals, const int32_t *b_col_ptr,
+                     const int32_t *b_row_idx, const double *b_vals, int64_t nnz_b, const int64_t *prod_ptr,
+                     int64_t total_products, int32_t *col_ptr, int32_t *row_idx, double *out_vals,
+                     int64_t *info, void *ws, size_t ws_bytes, int64_t *slice_nnz, int64_t *slice_offset,
+                     void *stream);
 
 /* ---------------------------------------------------------------------------
  * construction-funnelled ops and segmented reductions of the

@@ -336,6 +336,33 @@ def mg_spmm(n_rows, n_cols, csr, B, out=None):
     return C
 
 
+def mg_spgemm(n_rows_a, n_inner, n_cols_slice, a, b_slice):
+    """C[:, slice] = A @ B[:, slice] on this rank (b_slice: a standalone CSC of
+    the rank's columns of B) plus the all-gather of the slices' nnz.  Returns
+    (col_ptr, row_idx, vals, slice_nnz int64[world], slice_offset int64[1]) --
+    the last two stay on the device (dist.DistCsc)."""
+    L = _lib.lib()
+    a_ptr, a_rows, a_vals = a
+    b_ptr, b_rows, b_vals = b_slice
+    dev = a_ptr.device
+    prod_ptr, total = spgemm_products(n_rows_a, n_inner, n_cols_slice, a_ptr, b_ptr, b_rows)
+    cap = max(total, 1)
+    col_ptr = torch.empty(n_cols_slice + 1, dtype=torch.int32, device=dev)
+    row_idx = torch.empty(cap, dtype=torch.int32, device=dev)
+    out_vals = torch.empty(cap, dtype=torch.float64, device=dev)
+    info = torch.zeros(2, dtype=torch.int64, device=dev)
+    slice_nnz = torch.empty(max(L.as_mg_world(), 1), dtype=torch.int64, device=dev)
+    slice_off = torch.empty(1, dtype=torch.int64, device=dev)
+    nnz_b = int(b_rows.numel())
+    ws_bytes = L.as_spgemm_workspace_bytes(n_cols_slice, nnz_b, total)
+    ws = workspace(ws_bytes, dev)
+    check(L.as_mg_spgemm_f64(n_rows_a, n_inner, n_cols_slice, ptr(a_ptr), ptr(a_rows), ptr(a_vals), ptr(b_ptr),
+                             ptr(b_rows), ptr(b_vals), nnz_b, ptr(prod_ptr), total, ptr(col_ptr), ptr(row_idx),
+                             ptr(out_vals), ptr(info), ptr(ws), ws_bytes, ptr(slice_nnz), ptr(slice_off), stream()))
+    nnz = int(info[0].item())
+    return col_ptr, row_idx[:nnz], out_vals[:nnz], slice_nnz, slice_off
+
+
 def spmm_csc(n_rows, n_cols, csc, B, out=None):
     """C = A @ B straight over the CSC of A (column-merge, float32; no CSR
     needed): the reference's loop order (_kernels.mat_times_vec,

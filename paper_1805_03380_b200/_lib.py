@@ -61,6 +61,7 @@ SIGNATURES = {
     "as_mg_trace_workspace_bytes": (SZ, [I64, I64, I64, INT]),
     "as_mg_trace_atb_f64": (INT, [I64, I64, P, P, P, P, P, P, I64, I64, I64, I64, P, P, SZ, P]),
     "as_mg_spmm_csr_f32": (INT, [I64, I64, I64, P, P, P, P, I64, P, I64, P, SZ, P]),
+    "as_mg_spgemm_f64": (INT, [I64, I64, I64, P, P, P, P, P, P, I64, P, I64, P, P, P, P, P, SZ, P, P, P]),
     "as_trace_workspace_bytes": (SZ, [I64, I64, I64]),
     "as_trace_atb_f64": (INT, [I64, I64, P, P, P, P, P, P, I64, I64, P, P, SZ, P]),
     "as_expand_cols": (INT, [I64, P, P, P]),

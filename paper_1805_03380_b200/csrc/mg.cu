@@ -1,5 +1,5 @@
 // mg.cu -- multi-GPU entry points of the C ABI: the
-// column-sharded trace(A^T B) and SpMM as ONE call each -- the rank-local
+// column-sharded trace(A^T B), SpMM and SpGEMM as ONE call each -- the rank-local
 // kernel followed by its NCCL collective on the caller's stream -- for a host
 // that does not go through torch.distributed (paper_1805_03380_b200/dist.py
 // is the Python twin and the reference for the combination order).
@@ -22,10 +22,10 @@ namespace as {
 namespace {
 
 // the few NCCL entry points used (nccl.h: ncclResult_t is an int enum,
-// ncclSuccess = 0; ncclFloat32 = 7, ncclFloat64 = 8)
+// ncclSuccess = 0; ncclInt64 = 4, ncclFloat32 = 7, ncclFloat64 = 8)
 using nccl_all_gather_t = int (*)(const void*, void*, size_t, int, void*, cudaStream_t);
 using nccl_error_string_t = const char* (*)(int);
-constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8;
+constexpr int kNcclInt64 = 4, kNcclFloat32 = 7, kNcclFloat64 = 8;
 
 struct MgState {
   void* lib = nullptr;
@@ -73,6 +73,13 @@ __global__ void mg_dd_combine_kernel(const double* __restrict__ gathered, int wo
   const double total = __dadd_rn(s, e);
   out[0] = total;
   out[1] = __dsub_rn(e, __dsub_rn(total, s));
+}
+
+// this rank's first element in the concatenation of the ranks' slices
+__global__ void mg_slice_offset_kernel(const long long* __restrict__ slice_nnz, int rank, long long* __restrict__ off) {
+  long long s = 0;
+  for (int r = 0; r < rank; r++) s += slice_nnz[r];
+  off[0] = s;
 }
 
 constexpr size_t kMgSlots = 256;  // bytes reserved for one rank's partial in front of the gather buffer
@@ -164,6 +171,27 @@ int as_mg_spmm_csr_f32(int64_t n_rows, int64_t n_cols, int64_t k, const int32_t*
   if (rc != AS_OK) return rc;
   // in place: every rank's block lands in the same columns of every C
   AS_NCCL_TRY(g_mg.all_gather(C + k0 * ldc, C, (size_t)(kb * ldc), kNcclFloat32, g_mg.comm, st));
+  return AS_OK;
+}
+
+int as_mg_spgemm_f64(int64_t n_rows_a, int64_t n_inner, int64_t n_cols_b, const int32_t* a_col_ptr,
+                     const int32_t* a_row_idx, const double* a_vals, const int32_t* b_col_ptr, const int32_t* b_row_idx,
+                     const double* b_vals, int64_t nnz_b, const int64_t* prod_ptr, int64_t total_products,
+                     int32_t* col_ptr, int32_t* row_idx, double* out_vals, int64_t* info, void* ws, size_t ws_bytes,
+                     int64_t* slice_nnz, int64_t* slice_offset, void* stream) {
+  cudaStream_t st = S(stream);
+  AS_REQUIRE(g_mg.comm != nullptr, AS_ERR_ARG, "as_mg_init has not been called");
+  AS_REQUIRE(slice_nnz != nullptr && slice_offset != nullptr, AS_ERR_ARG, "null slice_nnz / slice_offset");
+  // the rank's column slice of B (a standalone CSC: dist.spgemm_shard cuts B into
+  // ranges of equal Gustavson products); A is replicated
+  const int rc = as_spgemm_f64(n_rows_a, n_inner, n_cols_b, a_col_ptr, a_row_idx, a_vals, b_col_ptr, b_row_idx, b_vals,
+                               nnz_b, prod_ptr, total_products, col_ptr, row_idx, out_vals, info, ws, ws_bytes, stream);
+  if (rc != AS_OK) return rc;
+  // C stays distributed: one all-gather of the slices' nnz (info[0], still on the
+  // device), each rank's global element offset by a scan in rank order
+  AS_NCCL_TRY(g_mg.all_gather(info, slice_nnz, 1, kNcclInt64, g_mg.comm, st));
+  mg_slice_offset_kernel<<<1, 1, 0, st>>>((const long long*)slice_nnz, g_mg.rank, (long long*)slice_offset);
+  AS_LAUNCH_CHECK();
   return AS_OK;
 }
 

@@ -112,3 +112,27 @@ def test_spmm_block_gather(K, comm, k):
     want = K.spmm(n_rows, n_cols, csr, X)
     got = K.mg_spmm(n_rows, n_cols, csr, X)
     assert torch.equal(got, want)
+
+
+def test_spgemm_slices_stay_distributed(K, comm):
+    from paper_1805_03380_b200 import dist as D
+
+    m, kk, n = 900, 700, 800
+    a, b = _rand_csc(5, m, kk, 9000), _rand_csc(6, kk, n, 8000)
+    want = oracle.spgemm(m, *a, *b, n)
+    da = _dev(a)
+    # the two ranks' column slices of B, one after the other (each a one-rank gather)
+    bounds = [0, 350, n]
+    got_vals, got_rows, got_ptr = [], [], [0]
+    for r in range(2):
+        c0, c1 = bounds[r], bounds[r + 1]
+        sl = D.csc_column_slice(np.asarray(b[2]), np.asarray(b[1]), np.asarray(b[0]), c0, c1)  # (ptr, rows, vals)
+        db = _dev((sl[2], sl[1], sl[0]))
+        p, ri, v, snnz, soff = K.mg_spgemm(m, kk, c1 - c0, da, db)
+        assert snnz.cpu().tolist() == [int(ri.shape[0])] and soff.cpu().tolist() == [0]
+        got_vals.append(v.cpu().numpy())
+        got_rows.append(ri.cpu().numpy())
+        got_ptr.extend((p.cpu().numpy()[1:].astype(np.int64) + got_ptr[-1]).tolist())
+    assert np.array_equal(np.asarray(got_ptr), want[2])
+    assert np.array_equal(np.concatenate(got_rows), want[1])
+    assert np.array_equal(np.concatenate(got_vals).view(np.int64), want[0].view(np.int64))
