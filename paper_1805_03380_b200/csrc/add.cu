@@ -364,6 +364,12 @@ __global__ void __launch_bounds__(kAddThreads, AS_ADD_MINB) add_tile_kernel(AddA
     }
     int total;
     const int off = block_exclusive_scan<int>(cnt, S.scan_i, &total);  // (its barriers end every merge)
+    // 3a. the count is known: publish it and take the next ticket before staging the
+    //     outputs, so the successors' look-backs find it that much earlier
+    if (tid == 0) {
+      atomicExch(&a.states[t], ((unsigned long long)total << 2) | (t == 0 ? kFlagInc : kFlagAgg));  // (no fence needed)
+      S.tile = (long long)atomicAdd(a.ticket, 1ull);
+    }
     {
       int run = off;
 #pragma unroll
@@ -378,12 +384,7 @@ __global__ void __launch_bounds__(kAddThreads, AS_ADD_MINB) add_tile_kernel(AddA
       if (tid == 0) S.excl[pad(n)] = (unsigned)total;
     }
 
-    // 3. publish the count, take the next ticket and start its loads, then
-    //    look back for the output offset and write
-    if (tid == 0) {
-      atomicExch(&a.states[t], ((unsigned long long)total << 2) | (t == 0 ? kFlagInc : kFlagAgg));  // (no fence needed)
-      S.tile = (long long)atomicAdd(a.ticket, 1ull);
-    }
+    // 3b. start the next tile's loads, then look back for the output offset and write
     __syncthreads();
     const long long tn = S.tile;
     if (tn < a.n_tiles) add_prefetch(a, tn, P);
