@@ -572,6 +572,9 @@ trace_warp_tile_kernel(long long n_cols, const int* __restrict__ ap, const int* 
     for (int o = 16; o > 0; o >>= 1) v = dd_merge(v, dd_shfl_xor(v, o));
     if (lane == 0) {
       partials[blockIdx.x] = v;
+      // launched with programmatic stream serialization behind the kernel that zeroes
+      // `done`: everything above overlapped it, the counter is first touched here
+      asm volatile("griddepcontrol.wait;" ::: "memory");
       __threadfence();
       const unsigned prev = atomicAdd(done, 1u);
       S.s_last = (prev == gridDim.x - 1);
@@ -594,6 +597,12 @@ trace_warp_tile_kernel(long long n_cols, const int* __restrict__ ap, const int* 
       out[1] = lo2;
     }
   }
+}
+
+// zeroes the last-block counter; the warp-tile kernel is launched behind it with
+// programmatic stream serialization (no memset node in front of the trace)
+__global__ void trace_zero_kernel(unsigned* done) {
+  if (threadIdx.x == 0) *done = 0u;
 }
 
 template <int LG>
@@ -650,7 +659,6 @@ int as_trace_atb_f64(int64_t n_rows, int64_t n_cols, const int32_t* a_col_ptr, c
   AS_REQUIRE(ws_bytes >= as_trace_workspace_bytes(n_cols, nnz_a, nnz_b), AS_ERR_ARG, "workspace too small");
   unsigned* done = (unsigned*)ws;
   DD* partials = (DD*)((char*)ws + 256);
-  AS_CUDA_TRY(cudaMemsetAsync(done, 0, sizeof(unsigned), st));
   // the warp-tile kernel's bulk copies need 16-byte aligned row arrays
   const bool aligned = (((uintptr_t)a_row_idx | (uintptr_t)b_row_idx) & 15u) == 0;
   const double mean = n_cols > 0 ? (double)(nnz_a + nnz_b) / (2.0 * (double)n_cols) : 0.0;
@@ -667,9 +675,20 @@ int as_trace_atb_f64(int64_t n_rows, int64_t n_cols, const int32_t* a_col_ptr, c
       const long long tiles = (n_cols + (32 >> LG) - 1) / (32 >> LG);                                             \
       const unsigned blocks =                                                                                     \
           (unsigned)std::min<long long>(std::min(grid, 148 * 32), (tiles + kTwWarps - 1) / kTwWarps);             \
-      trace_warp_tile_kernel<LG><<<blocks, kTwThreads, sizeof(TwSmem), st>>>(                                     \
-          n_cols, a_col_ptr, a_row_idx, a_vals, b_col_ptr, b_row_idx, b_vals, (int)nnz_a, (int)nnz_b, partials,   \
-          done, out);                                                                                             \
+      trace_zero_kernel<<<1, 32, 0, st>>>(done);                                                                  \
+      cudaLaunchConfig_t cfg = {};                                                                                \
+      cfg.gridDim = dim3(blocks);                                                                                 \
+      cfg.blockDim = dim3(kTwThreads);                                                                            \
+      cfg.dynamicSmemBytes = sizeof(TwSmem);                                                                      \
+      cfg.stream = st;                                                                                            \
+      cudaLaunchAttribute attr[1];                                                                                \
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                            \
+      attr[0].val.programmaticStreamSerializationAllowed = 1;                                                     \
+      cfg.attrs = attr;                                                                                           \
+      cfg.numAttrs = 1;                                                                                           \
+      AS_CUDA_TRY(cudaLaunchKernelEx(&cfg, trace_warp_tile_kernel<LG>, (long long)n_cols, a_col_ptr, a_row_idx,   \
+                                     a_vals, b_col_ptr, b_row_idx, b_vals, (int)nnz_a, (int)nnz_b, partials,      \
+                                     done, out));                                                                 \
     }                                                                                                             \
     break;
     switch (lg) {
@@ -686,6 +705,7 @@ int as_trace_atb_f64(int64_t n_rows, int64_t n_cols, const int32_t* a_col_ptr, c
       return AS_OK;
     }
   }
+  AS_CUDA_TRY(cudaMemsetAsync(done, 0, sizeof(unsigned), st));
   const long long blocks = std::min(trace_grid(), 148 * 32);
   trace_partial_kernel<<<(unsigned)blocks, kTrThreads, 0, st>>>(n_cols, a_col_ptr, a_row_idx, a_vals, b_col_ptr,
                                                                 b_row_idx, b_vals, partials, done, out);
