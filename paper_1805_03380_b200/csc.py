@@ -74,12 +74,18 @@ _STAGING_LOCK = threading.Lock()
 _STAGING = {}
 
 
+_STAGING_KEEP_BYTES = 256 << 20  # larger read-backs get their own buffers (not kept)
+
+
 def _staging(n_ptr: int, cap: int, val_dtype):
-    """Process-wide pinned read-back buffers (grow-only) for the host mirror."""
+    """Process-wide pinned read-back buffers (grow-only up to
+    _STAGING_KEEP_BYTES each) for the host mirror."""
     def grown(key, n, dtype):
         t = _STAGING.get(key)
         if t is None or t.shape[0] < n:
-            t = _STAGING[key] = torch.empty(max(n, 1) + max(n, 1) // 4, dtype=dtype, pin_memory=True)
+            t = torch.empty(max(n, 1) + max(n, 1) // 4, dtype=dtype, pin_memory=True)
+            if t.numel() * t.element_size() <= _STAGING_KEEP_BYTES:
+                _STAGING[key] = t
         return t
 
     return (grown("ptr", n_ptr, torch.int32)[:n_ptr], grown("rows", cap, torch.int32),
