@@ -35,7 +35,16 @@ static Plan plan(long long n, long long n_out_cols, int mb) {
   if (max_w > sr::kMaxW || bits_for(max_w - 1) + mb > 32) return p;
   p.ok = true;
   p.nb = nb;
-  p.lob = nb <= kR ? 0 : 8;
+  // two passes: the bucket id's bits split evenly between the low digit (pass A) and the
+  // high digit (pass B), so both passes scatter runs of similar length (with a fixed 8-bit
+  // low digit, 1e7 elements over 5,747 buckets gave pass A runs of 8 elements -- 9.4 store
+  // sectors per request -- and pass B runs of 89; build 1e7 473 -> 461 us, transpose 5e7
+  // 1.89 -> 1.83 ms)
+  static const int kLobEnv = getenv("AS_LN_LOB") ? atoi(getenv("AS_LN_LOB")) : 0;
+  const int bits = bits_for(nb - 1);
+  int lob = kLobEnv > 0 ? kLobEnv : bits / 2;
+  lob = std::min(8, std::max(lob, bits - 8));
+  p.lob = nb <= kR ? 0 : lob;
   p.T_ = (n + kE - 1) / kE;
   p.cb_mul = (unsigned long long)((((unsigned __int128)nb) << 32) / (unsigned long long)n_out_cols);
   return p;
