@@ -13,7 +13,7 @@ namespace as {
 namespace ln {
 
 constexpr long long kMaxBuckets = (long long)kR * kR;
-constexpr double kFill = 0.85;
+static const double kFill = getenv("AS_LN_FILL") ? atof(getenv("AS_LN_FILL")) : 0.85;  // mean bucket size / tile
 
 struct Plan {
   bool ok = false;
