@@ -232,8 +232,8 @@ __device__ __forceinline__ void add_prefetch(const AddArgs& a, long long t, AddP
 }
 
 // Persistent: each CTA takes tiles by ticket until none is left.  The next
-// tile's ticket is taken as soon as this tile's count is published, and its
-// inputs are in flight while this tile looks back and writes.
+// tile's ticket is taken when this tile starts, and its inputs are in flight
+// while this tile looks back and writes.
 __global__ void __launch_bounds__(kAddThreads, AS_ADD_MINB) add_tile_kernel(AddArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   AddSmem& S = *reinterpret_cast<AddSmem*>(smem_raw);
@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(kAddThreads, AS_ADD_MINB) add_tile_kernel(AddA
   long long t = S.tile;
   AddPrefetch P;
   if (t < a.n_tiles) add_prefetch(a, t, P);
+  __syncthreads();  // S.tile is rewritten at the start of the first tile
   while (t < a.n_tiles) {
     const AddDesc d0 = P.d0, d1 = P.d1;
     const long long c_first = d0.col, c_last = P.c_last, own_lo = P.own_lo;
@@ -252,6 +253,9 @@ __global__ void __launch_bounds__(kAddThreads, AS_ADD_MINB) add_tile_kernel(AddA
     const int na = d1.ia - ia0, nb = d1.jb - jb0, n = na + nb;
     const long long tpos = t * kAddTile;
     const long long span = c_last - c_first + 1;
+    // the next ticket is claimed now (read behind this tile's first barrier), so its loads
+    // can be issued as soon as the merge's registers are free -- no barrier in between
+    if (tid == 0) S.tile = (long long)atomicAdd(a.ticket, 1ull);
 
     // 1. rows, values and the column starts of the tile's A and B ranges
 #pragma unroll
@@ -284,6 +288,7 @@ __global__ void __launch_bounds__(kAddThreads, AS_ADD_MINB) add_tile_kernel(AddA
       if (span <= kAddTile) S.cms[k] = (int)((long long)as_ + bs - tpos);
     }
     __syncthreads();
+    const long long tn = S.tile;
     {  // columns: inclusive max-scan of the marks (B's marks dominate A's); marks re-zeroed
       const int e0 = tid * kAddItems;
       unsigned m[kAddItems];
@@ -366,10 +371,8 @@ __global__ void __launch_bounds__(kAddThreads, AS_ADD_MINB) add_tile_kernel(AddA
     const int off = block_exclusive_scan<int>(cnt, S.scan_i, &total);  // (its barriers end every merge)
     // 3a. the count is known: publish it and take the next ticket before staging the
     //     outputs, so the successors' look-backs find it that much earlier
-    if (tid == 0) {
+    if (tid == 0)
       atomicExch(&a.states[t], ((unsigned long long)total << 2) | (t == 0 ? kFlagInc : kFlagAgg));  // (no fence needed)
-      S.tile = (long long)atomicAdd(a.ticket, 1ull);
-    }
     {
       int run = off;
 #pragma unroll
@@ -385,8 +388,6 @@ __global__ void __launch_bounds__(kAddThreads, AS_ADD_MINB) add_tile_kernel(AddA
     }
 
     // 3b. start the next tile's loads, then look back for the output offset and write
-    __syncthreads();
-    const long long tn = S.tile;
     if (tn < a.n_tiles) add_prefetch(a, tn, P);
     if (tid < 32) {
       const unsigned long long pre = add_lookback_wait(a.states, t, (unsigned long long)total);
